@@ -1,0 +1,175 @@
+"""Parity oracle for the EvoGP hot path — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this package. The product package
+(paper_2501_17168_b200) never imports it, and it never imports the product.
+
+Thin ctypes wrappers over oracle.c (plain C, FP64) plus the certificate
+decision rules of DESIGN.md reading R14:
+  * a point is *certified* iff every decision on its path is robust, its FP64
+    value is finite and 2*e <= 0.5 * tol * max(1, |v|);
+  * a tree is *MSE-certified* iff all its points are certified and
+    2 * sum_d (2|v_d - y_d| e_d + e_d^2) <= 0.5 * tol * SSE.
+Parity of each function is pinned by tests/test_oracle_pins.py (no GPU).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+OK, E_ARG, E_TOO_LARGE, E_MALFORMED, E_VAR_RANGE, E_FUNC_UNKNOWN, E_OUT_RANGE = 0, -1, -2, -3, -4, -5, -6
+
+TOL = 1e-4  # north star: |gpu - oracle| <= 1e-4 * max(1, |oracle|)
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "oracle.c")
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+        # plain -O2, no -ffast-math, no FMA contraction: the oracle computes
+        # exactly the expressions written in oracle.c
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+                               "-pthread", "-o", _SO, src, "-lm"])
+    return _SO
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_SO)
+            i64, i32, vp = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p
+            lib.oracle_tensorize.argtypes = [i64, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp]
+            lib.oracle_tensorize.restype = ctypes.c_int
+            lib.oracle_eval.argtypes = [vp, vp, vp, i64, i32, vp, i64, i32, i32, i32, vp, vp, vp, i32]
+            lib.oracle_eval.restype = ctypes.c_int
+            lib.oracle_eval_recursive.argtypes = [vp, vp, i32, vp, i32, i32, i32, vp]
+            lib.oracle_eval_recursive.restype = ctypes.c_int
+            lib.oracle_mse.argtypes = [vp, vp, i64, i64, vp]
+            lib.oracle_mse.restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def _p(a):
+    return ctypes.c_void_p(a.ctypes.data) if a is not None else None
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status, tree=-1, node=-1):
+        super().__init__(f"oracle status {status} (tree {tree}, node {node})")
+        self.status, self.tree, self.node = status, tree, node
+
+
+def tensorize(offsets, types, values, max_len: int, n_inputs: int, n_outputs: int = 1, raise_on_error=True):
+    """Prefix CSR -> (type[P,L] i16, value[P,L] f32, size[P,L] i16). PAPER.md P:221-258."""
+    lib = _load()
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    types = np.ascontiguousarray(types, dtype=np.int16)
+    values = np.ascontiguousarray(values, dtype=np.float32)
+    P = len(offsets) - 1
+    ot = np.zeros((P, max_len), dtype=np.int16)
+    ov = np.zeros((P, max_len), dtype=np.float32)
+    os_ = np.zeros((P, max_len), dtype=np.int16)
+    et = np.zeros(1, dtype=np.int64)
+    en = np.zeros(1, dtype=np.int32)
+    if types.size == 0:
+        types = np.zeros(1, dtype=np.int16)
+        values = np.zeros(1, dtype=np.float32)
+    st = lib.oracle_tensorize(P, _p(offsets), _p(types), _p(values), max_len, n_inputs, n_outputs,
+                              _p(ot), _p(ov), _p(os_), _p(et), _p(en))
+    if st != OK:
+        if raise_on_error:
+            raise OracleError(st, int(et[0]), int(en[0]))
+        return st, int(et[0]), int(en[0])
+    return (ot, ov, os_) if raise_on_error else (OK, -1, -1, ot, ov, os_)
+
+
+def evaluate(type_, value, size, X, n_out: int = 1, mode: int = 0, certify: bool = False,
+             threads: int | None = None):
+    """Stack evaluation. Returns out[P,D,n_out] float64 (and err, robust
+    if certify). mode 0 = FP64 + FP32-range emulation; 1 = FP32-faithful."""
+    lib = _load()
+    type_ = np.ascontiguousarray(type_, dtype=np.int16)
+    value = np.ascontiguousarray(value, dtype=np.float32)
+    size = np.ascontiguousarray(size, dtype=np.int16)
+    X = np.ascontiguousarray(X, dtype=np.float32)
+    P, ld = type_.shape
+    D, n_in = X.shape
+    out = np.zeros((P, D, n_out), dtype=np.float64)
+    err = np.zeros((P, D, n_out), dtype=np.float64) if certify else None
+    rob = np.zeros((P, D, n_out), dtype=np.uint8) if certify else None
+    th = threads or min(32, os.cpu_count() or 1)
+    st = lib.oracle_eval(_p(type_), _p(value), _p(size), P, ld, _p(X), D, n_in, n_out, mode, _p(out),
+                         _p(err), _p(rob), th)
+    if st != OK:
+        raise OracleError(st)
+    if certify:
+        return out, err, rob.astype(bool)
+    return out
+
+
+def evaluate_recursive(types, values, x, n_out: int = 1, mode: int = 0):
+    """Independent recursive interpreter for one unpadded prefix tree at one point."""
+    lib = _load()
+    types = np.ascontiguousarray(types, dtype=np.int16)
+    values = np.ascontiguousarray(values, dtype=np.float32)
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.zeros(n_out, dtype=np.float64)
+    st = lib.oracle_eval_recursive(_p(types), _p(values), len(types), _p(x), len(x), n_out, mode, _p(out))
+    if st != OK:
+        raise OracleError(st)
+    return out
+
+
+def mse(pred, y):
+    """mse[p] = mean_d (pred[p,d] - y[d])^2 in FP64 (reading R7)."""
+    lib = _load()
+    pred = np.ascontiguousarray(pred, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    P = pred.shape[0]
+    D = pred.shape[1]
+    out = np.zeros(P, dtype=np.float64)
+    st = lib.oracle_mse(_p(pred.reshape(P, D)), _p(y), P, D, _p(out))
+    if st != OK:
+        raise OracleError(st)
+    return out
+
+
+def certified_points(v, e, robust, tol: float = TOL):
+    """Reading R14: robust decisions, finite value, 2e <= 0.5*tol*max(1,|v|)."""
+    with np.errstate(invalid="ignore", over="ignore"):
+        return robust & np.isfinite(v) & np.isfinite(e) & (2.0 * e <= 0.5 * tol * np.maximum(1.0, np.abs(v)))
+
+
+def mse_certified_trees(v, e, robust, y, tol: float = TOL):
+    """v, e, robust: [P, D] (single output). Returns bool[P]."""
+    cert = certified_points(v, e, robust, tol).all(axis=1)
+    with np.errstate(invalid="ignore", over="ignore"):
+        r = np.abs(v - y.astype(np.float64)[None, :])
+        bound = 2.0 * np.sum(2.0 * r * e + e * e, axis=1)
+        sse = np.sum(r * r, axis=1)
+        return cert & np.isfinite(sse) & (bound <= 0.5 * tol * sse)
+
+
+def within_tol(gpu, ref, tol: float = TOL):
+    """North-star per-point check with identical NaN/+-Inf class."""
+    gpu = np.asarray(gpu, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    same_nan = np.isnan(gpu) == np.isnan(ref)
+    inf_g = np.isinf(gpu)
+    inf_r = np.isinf(ref)
+    same_inf = (inf_g == inf_r) & (~inf_g | (np.sign(gpu) == np.sign(ref)))
+    fin = np.isfinite(gpu) & np.isfinite(ref)
+    with np.errstate(invalid="ignore", over="ignore"):
+        close = np.abs(gpu - ref) <= tol * np.maximum(1.0, np.abs(ref))
+    return same_nan & same_inf & (~fin | close)
