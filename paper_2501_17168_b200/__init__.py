@@ -1,0 +1,195 @@
+"""paper_2501_17168_b200 — B200-native (sm_100a) EvoGP hot path.
+
+Thin Python binding over libevogp.so (include/evogp.h). Every step of the
+path runs in the library's CUDA kernels; this module only marshals
+arguments (torch is used for device memory and streams). Names follow the
+C-ABI: ``tensorize``, ``eval``, ``sr_fitness``, ``sr_sse``,
+``select_strategy``, ``workspace_size``, ``check_device_flags``.
+
+Population arrays are the paper's tensorized layout (§III-A,
+P:221-258): ``type`` int16, ``value`` float32, ``size`` int16, each P x ld.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import (E_ARG, E_CUDA, E_FUNC_UNKNOWN, E_MALFORMED, E_OUT_RANGE, E_TOO_LARGE, E_UNSUPPORTED,
+                   E_VAR_RANGE, OK, STRATEGY_AUTO, STRATEGY_INTER, STRATEGY_INTRA, X_ROWMAJOR, X_SOA)
+
+_LIB = _lib.load()
+
+__all__ = [
+    "tensorize", "eval", "sr_fitness", "sr_sse", "select_strategy", "workspace_size", "Workspace",
+    "check_device_flags", "EvogpError", "last_launch_count", "STRATEGIES",
+]
+
+STRATEGIES = {"auto": STRATEGY_AUTO, "inter": STRATEGY_INTER, "intra": STRATEGY_INTRA,
+              STRATEGY_AUTO: STRATEGY_AUTO, STRATEGY_INTER: STRATEGY_INTER, STRATEGY_INTRA: STRATEGY_INTRA}
+
+
+class EvogpError(RuntimeError):
+    def __init__(self, status: int, where: str, tree: int = -1, node: int = -1):
+        msg = _LIB.evogp_status_string(status).decode()
+        detail = _LIB.evogp_last_error().decode()
+        super().__init__(f"{where}: {msg} ({status}); {detail}; tree={tree} node={node}")
+        self.status, self.tree, self.node = status, tree, node
+
+
+def _vp(a) -> ctypes.c_void_p:
+    if a is None:
+        return ctypes.c_void_p(0)
+    if isinstance(a, np.ndarray):
+        return ctypes.c_void_p(a.ctypes.data)
+    return ctypes.c_void_p(a.data_ptr())
+
+
+def tensorize(offsets, types, values, max_len: int, n_inputs: int, n_outputs: int = 1):
+    """Host: prefix CSR lists -> (type[P,L] int16, value[P,L] float32, size[P,L] int16)."""
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    types = np.ascontiguousarray(types, dtype=np.int16)
+    values = np.ascontiguousarray(values, dtype=np.float32)
+    P = len(offsets) - 1
+    ot = np.empty((P, max_len), dtype=np.int16)
+    ov = np.empty((P, max_len), dtype=np.float32)
+    osz = np.empty((P, max_len), dtype=np.int16)
+    et = np.zeros(1, dtype=np.int64)
+    en = np.zeros(1, dtype=np.int32)
+    if types.size == 0:
+        types = np.zeros(1, np.int16)
+        values = np.zeros(1, np.float32)
+    st = _LIB.evogp_tensorize(P, _vp(offsets), _vp(types), _vp(values), max_len, n_inputs, n_outputs, _vp(ot),
+                              _vp(ov), _vp(osz), _vp(et), _vp(en))
+    if st != OK:
+        raise EvogpError(st, "evogp_tensorize", int(et[0]), int(en[0]))
+    return ot, ov, osz
+
+
+def workspace_size(P: int, D: int, max_len: int, n_inputs: int, n_outputs: int = 1) -> int:
+    return int(_LIB.evogp_workspace_size(P, D, max_len, n_inputs, n_outputs))
+
+
+class Workspace:
+    """Zero-initialised device scratch sized by evogp_workspace_size."""
+
+    def __init__(self, P, D, max_len, n_inputs, n_outputs=1, device=None):
+        import torch
+
+        self.nbytes = workspace_size(P, D, max_len, n_inputs, n_outputs)
+        self.buf = torch.zeros(self.nbytes + 256, dtype=torch.uint8, device=device)
+        base = self.buf.data_ptr()
+        self.ptr = (base + 255) // 256 * 256
+        self.key = (P, D, max_len, n_inputs, n_outputs, str(self.buf.device))
+
+
+_WS_CACHE: dict = {}
+
+
+def _workspace(P, D, L, n_in, n_out, device, ws):
+    if ws is not None:
+        return ws
+    key = (P, D, L, n_in, n_out, str(device))
+    w = _WS_CACHE.get(key)
+    if w is None:
+        if len(_WS_CACHE) > 16:
+            _WS_CACHE.clear()
+        w = Workspace(P, D, L, n_in, n_out, device)
+        _WS_CACHE[key] = w
+    return w
+
+
+def _stream_ptr(stream, device):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _tree_args(type_, value, size, max_len):
+    P, ld = int(type_.shape[0]), int(type_.shape[1])
+    L = ld if max_len is None else int(max_len)
+    for t in (type_, value, size):
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("tree arrays must be contiguous CUDA tensors")
+    return P, L, ld
+
+
+def _x_args(X, x_layout):
+    lay = X_SOA if x_layout in ("soa", X_SOA) else X_ROWMAJOR
+    if not X.is_cuda or not X.is_contiguous():
+        raise ValueError("X must be a contiguous CUDA tensor")
+    if lay == X_ROWMAJOR:
+        D, n_in = int(X.shape[0]), int(X.shape[1])
+    else:
+        n_in, D = int(X.shape[0]), int(X.shape[1])
+    return lay, D, n_in
+
+
+def eval(type_, value, size, X, n_outputs: int = 1, strategy="auto", x_layout="rowmajor", max_len=None,
+         out=None, workspace: Workspace | None = None, stream=None):
+    """Device: out[P, D, n_outputs] float32 (Modi P:391-411)."""
+    import torch
+
+    P, L, ld = _tree_args(type_, value, size, max_len)
+    lay, D, n_in = _x_args(X, x_layout)
+    if out is None:
+        out = torch.empty((P, D, n_outputs), dtype=torch.float32, device=X.device)
+    ws = _workspace(P, D, L, n_in, n_outputs, X.device, workspace)
+    st = _LIB.evogp_eval(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(X), D, n_in, lay, n_outputs, _vp(out),
+                         STRATEGIES[strategy], ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream, X.device))
+    if st != OK:
+        raise EvogpError(st, "evogp_eval")
+    return out
+
+
+def _sr(fn, name, type_, value, size, X, y, strategy, x_layout, max_len, out, workspace, stream):
+    import torch
+
+    P, L, ld = _tree_args(type_, value, size, max_len)
+    lay, D, n_in = _x_args(X, x_layout)
+    if not y.is_cuda or y.dtype != torch.float32 or y.numel() != D:
+        raise ValueError("y must be a float32 CUDA tensor of length D")
+    if out is None:
+        out = torch.empty(P, dtype=torch.float64, device=X.device)
+    ws = _workspace(P, D, L, n_in, 1, X.device, workspace)
+    st = fn(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(X), D, n_in, lay, _vp(y), _vp(out),
+            STRATEGIES[strategy], ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream, X.device))
+    if st != OK:
+        raise EvogpError(st, name)
+    return out
+
+
+def sr_fitness(type_, value, size, X, y, strategy="auto", x_layout="rowmajor", max_len=None, out=None,
+               workspace: Workspace | None = None, stream=None):
+    """Device: fused SR fitness mse[P] float64."""
+    return _sr(_LIB.evogp_sr_fitness, "evogp_sr_fitness", type_, value, size, X, y, strategy, x_layout, max_len,
+               out, workspace, stream)
+
+
+def sr_sse(type_, value, size, X, y, strategy="auto", x_layout="rowmajor", max_len=None, out=None,
+           workspace: Workspace | None = None, stream=None):
+    """Device: un-normalised sse[P] float64 for datapoint sharding."""
+    return _sr(_LIB.evogp_sr_sse, "evogp_sr_sse", type_, value, size, X, y, strategy, x_layout, max_len, out,
+               workspace, stream)
+
+
+def select_strategy(P: int, D: int, max_len: int, n_outputs: int = 1, device: int = 0) -> str:
+    s = _LIB.evogp_select_strategy(P, D, max_len, n_outputs, device)
+    if s < 0:
+        raise EvogpError(s, "evogp_select_strategy")
+    return "inter" if s == STRATEGY_INTER else "intra"
+
+
+def check_device_flags(workspace: Workspace, stream=None) -> int:
+    flags = np.zeros(1, dtype=np.int32)
+    st = _LIB.evogp_check_device_flags(ctypes.c_void_p(workspace.ptr), _stream_ptr(stream, workspace.buf.device),
+                                       _vp(flags))
+    if st != OK:
+        raise EvogpError(st, "evogp_check_device_flags")
+    return int(flags[0])
+
+
+def last_launch_count() -> int:
+    return int(_LIB.evogp_last_launch_count())

@@ -1,0 +1,189 @@
+// capi.cu — the extern "C" surface of libevogp.so (declared in include/evogp.h):
+// argument checks, planning (selector c), workspace carving, launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "evogp_internal.h"
+
+namespace evogp {
+
+namespace {
+thread_local char t_last_error[512] = "no error";
+thread_local int32_t t_last_launches = 0;
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    dev = 0;
+  }
+  return dev;
+}
+
+int fail(int status, const char* msg) {
+  set_last_error(msg);
+  return status;
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+int check_common(const int16_t* type, const float* value, const int16_t* size, int64_t P, int32_t max_len, int32_t ld,
+                 const float* X, int64_t D, int32_t n_inputs, int32_t x_layout, int32_t n_outputs, void* workspace) {
+  if (P < 0) return fail(EVOGP_E_ARG, "P < 0");
+  if (max_len < 1 || ld < max_len) return fail(EVOGP_E_ARG, "need 1 <= max_len <= ld");
+  if (max_len > kMaxLenSupported) return fail(EVOGP_E_UNSUPPORTED, "max_len > 8192 not supported");
+  if (D < 1 || D > (int64_t(1) << 40)) return fail(EVOGP_E_ARG, "D out of range");
+  if (n_inputs < 1 || n_inputs > kMaxInputs) return fail(EVOGP_E_ARG, "n_inputs out of range");
+  if (n_outputs < 1 || n_outputs > kMaxOutputs) return fail(EVOGP_E_ARG, "n_outputs out of range");
+  if (x_layout != EVOGP_X_ROWMAJOR && x_layout != EVOGP_X_SOA) return fail(EVOGP_E_ARG, "bad x_layout");
+  if (P > 0 && (!type || !value || !size)) return fail(EVOGP_E_ARG, "null tree array");
+  if (!X) return fail(EVOGP_E_ARG, "null X");
+  if (!workspace || !aligned(workspace, 256)) return fail(EVOGP_E_ARG, "workspace must be non-null, 256B aligned");
+  if (!aligned(value, 4) || !aligned(type, 2) || !aligned(size, 2) || !aligned(X, 4))
+    return fail(EVOGP_E_ARG, "misaligned array");
+  return EVOGP_OK;
+}
+
+int run(int mode, const int16_t* type, const float* value, const int16_t* size, int64_t P, int32_t max_len,
+        int32_t ld, const float* X, int64_t D, int32_t n_inputs, int32_t x_layout, int32_t n_outputs, float* out,
+        const float* y, double* res, int div_by_D, int32_t strategy, void* workspace, size_t ws_bytes,
+        void* stream) {
+  t_last_launches = 0;
+  if (strategy < EVOGP_STRATEGY_AUTO || strategy > EVOGP_STRATEGY_INTRA) return fail(EVOGP_E_ARG, "bad strategy");
+  Plan pl;
+  int st = plan_problem(pl, P, max_len, D, n_inputs, n_outputs, mode, strategy, current_device());
+  if (st != EVOGP_OK) return fail(st, "no launch plan for this shape");
+  if (ws_bytes < pl.total) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "workspace too small: %zu < %zu bytes", ws_bytes, pl.total);
+    return fail(EVOGP_E_ARG, buf);
+  }
+  if (P == 0) return EVOGP_OK;
+  unsigned char* ws = static_cast<unsigned char*>(workspace);
+  KParams& kp = pl.kp;
+  kp.type = type;
+  kp.value = value;
+  kp.size = size;
+  kp.ld = ld;
+  kp.xs = reinterpret_cast<const float*>(ws + pl.off_xs);
+  kp.y = y;
+  kp.out = out;
+  kp.res = res;
+  kp.div_by_D = div_by_D;
+  kp.flags = reinterpret_cast<int32_t*>(ws + pl.off_flags);
+  kp.counters = reinterpret_cast<int32_t*>(ws + pl.off_counters);
+  kp.partials = reinterpret_cast<double*>(ws + pl.off_partials);
+  kp.spill = reinterpret_cast<float*>(ws + pl.off_spill);
+  kp.use_tma = (ld % 8 == 0) && aligned(type, 16) && aligned(value, 16);
+  int nl = 0;
+  st = launch(pl, mode, X, x_layout, stream, &nl);
+  t_last_launches = nl;
+  return st;
+}
+
+}  // namespace
+
+void set_last_error(const char* msg) {
+  std::strncpy(t_last_error, msg, sizeof(t_last_error) - 1);
+  t_last_error[sizeof(t_last_error) - 1] = 0;
+}
+
+}  // namespace evogp
+
+using namespace evogp;
+
+extern "C" size_t evogp_workspace_size(int64_t P, int64_t D, int32_t max_len, int32_t n_inputs, int32_t n_outputs) {
+  if (P < 0 || D < 1 || max_len < 1 || max_len > kMaxLenSupported || n_inputs < 1 || n_outputs < 1) return 0;
+  const int dev = current_device();
+  size_t best = 256;
+  const int modes[2] = {n_outputs > 1 ? MODE_EVALN : MODE_EVAL1, MODE_SSE};
+  for (int m = 0; m < (n_outputs > 1 ? 1 : 2); ++m) {
+    for (int s = EVOGP_STRATEGY_INTER; s <= EVOGP_STRATEGY_INTRA; ++s) {
+      Plan pl;
+      if (plan_problem(pl, P, max_len, D, n_inputs, n_outputs, modes[m], s, dev) == EVOGP_OK)
+        best = std::max(best, pl.total);
+    }
+  }
+  return best;
+}
+
+extern "C" int evogp_eval(const int16_t* type, const float* value, const int16_t* size, int64_t P, int32_t max_len,
+                          int32_t ld, const float* X, int64_t D, int32_t n_inputs, int32_t x_layout,
+                          int32_t n_outputs, float* out, int32_t strategy, void* workspace, size_t ws_bytes,
+                          void* stream) {
+  int st = check_common(type, value, size, P, max_len, ld, X, D, n_inputs, x_layout, n_outputs, workspace);
+  if (st != EVOGP_OK) return st;
+  if (P > 0 && !out) return fail(EVOGP_E_ARG, "null out");
+  return run(n_outputs > 1 ? MODE_EVALN : MODE_EVAL1, type, value, size, P, max_len, ld, X, D, n_inputs, x_layout,
+             n_outputs, out, nullptr, nullptr, 0, strategy, workspace, ws_bytes, stream);
+}
+
+static int sr_common(const int16_t* type, const float* value, const int16_t* size, int64_t P, int32_t max_len,
+                     int32_t ld, const float* X, int64_t D, int32_t n_inputs, int32_t x_layout, const float* y,
+                     double* res, int div, int32_t strategy, void* workspace, size_t ws_bytes, void* stream) {
+  int st = check_common(type, value, size, P, max_len, ld, X, D, n_inputs, x_layout, 1, workspace);
+  if (st != EVOGP_OK) return st;
+  if (!y || (P > 0 && !res)) return fail(EVOGP_E_ARG, "null y / result");
+  return run(MODE_SSE, type, value, size, P, max_len, ld, X, D, n_inputs, x_layout, 1, nullptr, y, res, div,
+             strategy, workspace, ws_bytes, stream);
+}
+
+extern "C" int evogp_sr_fitness(const int16_t* type, const float* value, const int16_t* size, int64_t P,
+                                int32_t max_len, int32_t ld, const float* X, int64_t D, int32_t n_inputs,
+                                int32_t x_layout, const float* y, double* mse, int32_t strategy, void* workspace,
+                                size_t ws_bytes, void* stream) {
+  return sr_common(type, value, size, P, max_len, ld, X, D, n_inputs, x_layout, y, mse, 1, strategy, workspace,
+                   ws_bytes, stream);
+}
+
+extern "C" int evogp_sr_sse(const int16_t* type, const float* value, const int16_t* size, int64_t P, int32_t max_len,
+                            int32_t ld, const float* X, int64_t D, int32_t n_inputs, int32_t x_layout,
+                            const float* y, double* sse, int32_t strategy, void* workspace, size_t ws_bytes,
+                            void* stream) {
+  return sr_common(type, value, size, P, max_len, ld, X, D, n_inputs, x_layout, y, sse, 0, strategy, workspace,
+                   ws_bytes, stream);
+}
+
+extern "C" int evogp_select_strategy(int64_t P, int64_t D, int32_t max_len, int32_t n_outputs, int32_t device) {
+  if (P < 0 || D < 1 || max_len < 1 || n_outputs < 1) return EVOGP_E_ARG;
+  return select_strategy(P, D, max_len, n_outputs, device);
+}
+
+extern "C" int evogp_check_device_flags(void* workspace, void* stream, int32_t* flags) {
+  if (!workspace || !flags) return fail(EVOGP_E_ARG, "null workspace/flags");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t host = 0;
+  cudaError_t e = cudaMemcpyAsync(&host, workspace, 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(workspace, 0, 4, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    char buf[256];
+    std::snprintf(buf, sizeof(buf), "check_device_flags: %s", cudaGetErrorString(e));
+    return fail(EVOGP_E_CUDA, buf);
+  }
+  *flags = host;
+  return EVOGP_OK;
+}
+
+extern "C" const char* evogp_status_string(int status) {
+  switch (status) {
+    case EVOGP_OK: return "ok";
+    case EVOGP_E_ARG: return "invalid argument";
+    case EVOGP_E_TOO_LARGE: return "tree longer than max_len";
+    case EVOGP_E_MALFORMED: return "malformed tree";
+    case EVOGP_E_VAR_RANGE: return "variable index out of range";
+    case EVOGP_E_FUNC_UNKNOWN: return "unknown function id";
+    case EVOGP_E_OUT_RANGE: return "Modi output slot out of range";
+    case EVOGP_E_CUDA: return "CUDA error";
+    case EVOGP_E_UNSUPPORTED: return "unsupported configuration";
+  }
+  return "unknown status";
+}
+
+extern "C" const char* evogp_last_error(void) { return t_last_error; }
+
+extern "C" int32_t evogp_last_launch_count(void) { return t_last_launches; }

@@ -1,0 +1,100 @@
+// evogp_internal.h — library-internal definitions shared by the host C-ABI
+// (capi.cu, tensorize.cpp) and the kernels (kernels.cu). Not part of the ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/evogp.h"
+
+#ifdef __CUDACC__
+#define EVOGP_HD __host__ __device__
+#else
+#define EVOGP_HD
+#endif
+
+namespace evogp {
+
+constexpr int kNumFuncs = 22;
+constexpr int kMaxLenSupported = 8192;
+constexpr int kMaxInputs = 4096;
+constexpr int kMaxOutputs = 256;
+
+// Function ids (include/evogp.h, reading R3)
+enum Func : int {
+  F_ADD = 0, F_SUB, F_MUL, F_DIV, F_SIN, F_COS, F_TAN, F_MAX, F_MIN, F_POW, F_LOG,
+  F_EXP, F_TANH, F_NEG, F_ABS, F_SQRT, F_INV, F_LT, F_GT, F_LE, F_GE, F_IF
+};
+
+// Arity per function id; kind word = 1 + arity for function nodes.
+EVOGP_HD constexpr int func_arity(int f) {
+  return (f == F_SIN || f == F_COS || f == F_TAN || (f >= F_LOG && f <= F_INV)) ? 1 : (f == F_IF ? 3 : 2);
+}
+
+// Pre-decoded node word staged in shared memory (8 bytes, one LDS.64).
+// op: 0 CONST, 1 VAR, 2 + function id.  slot: Modi output slot or 0xFF.
+// arg: VAR input index.  val: CONST literal.
+enum : uint8_t { OP_CONST = 0, OP_VAR = 1, OP_FN = 2 };
+constexpr uint8_t kNoSlot = 0xFF;
+struct alignas(8) Node {
+  uint8_t op;
+  uint8_t slot;
+  uint16_t arg;
+  float val;
+};
+
+enum Mode : int { MODE_EVAL1 = 0, MODE_EVALN = 1, MODE_SSE = 2 };
+
+// Everything a kernel launch needs; built by plan() on the host.
+struct KParams {
+  const int16_t* type;
+  const float* value;
+  const int16_t* size;
+  int64_t P;
+  int32_t L;   // max_len
+  int32_t ld;  // row stride
+  int32_t n_in;
+  int32_t n_out;
+  int64_t D;
+  int64_t Dpad;
+  const float* xs;  // staged SoA X: n_in x Dpad
+  const float* y;
+  float* out;       // eval outputs
+  double* res;      // mse or sse
+  int32_t div_by_D; // 1: mse, 0: sse
+  int32_t nch;      // chunks of 32*K points per tree
+  int32_t nparts;   // partial sums per tree (inter: nch, intra: nseg)
+  int32_t nseg;     // intra: segments per tree
+  int32_t seg_chunks;
+  int32_t SD;          // shared-memory stack slots per warp
+  int32_t spill_slots; // global spill slots per warp
+  int32_t tree_bytes;  // per-warp (inter) or per-CTA (intra) decoded-tree bytes
+  int32_t warp_smem_bytes;
+  int32_t raw_bytes;   // intra: raw row staging bytes (type + value), 16B multiple
+  int32_t use_tma;     // intra: rows are 16B aligned -> cp.async.bulk staging
+  int32_t out_magic;   // ceil(2^32 / n_out) for index split in the Modi store
+  double* partials;
+  int32_t* counters;
+  int32_t* flags;
+  float* spill;
+};
+
+struct Plan {
+  int strategy;  // EVOGP_STRATEGY_INTER / _INTRA
+  int K;
+  int warps_per_cta;
+  int grid;
+  size_t smem_bytes;
+  KParams kp;
+  // workspace layout
+  size_t off_flags, off_xs, off_counters, off_partials, off_spill, total;
+};
+
+// kernels.cu
+int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_t n_out, int mode, int strategy,
+                 int device);
+int launch(Plan& pl, int mode, const float* X, int32_t x_layout, void* stream, int* n_launches);
+int select_strategy(int64_t P, int64_t D, int32_t L, int32_t n_out, int device);
+
+void set_last_error(const char* msg);
+
+}  // namespace evogp

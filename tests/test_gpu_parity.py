@@ -1,0 +1,406 @@
+"""GPU parity: the CUDA path through the C-ABI vs the oracle (DESIGN.md
+"Parity contract"):
+
+  Tier A (IEEE-exact mix): GPU outputs == oracle FP32-faithful replay bit for
+          bit (modulo +-0, NaN by class); within 1e-4*max(1,|o64|) of the FP64
+          oracle with identical NaN/Inf class; MSE within 1e-4 relative.
+  Tier B (paper / bounded / full mixes): every certified point within the
+          north-star tolerance with identical class; every MSE-certified tree
+          within 1e-4; literal pass rates reported (and sanity-bounded).
+  Tier C: fused sr_fitness == FP64 recompute from the GPU's own eval outputs.
+  Tier D: kernel (a) == kernel (b) bit for bit.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def _evogp():
+    import paper_2501_17168_b200 as evogp
+
+    return evogp
+
+
+def make_case(seed, P, L, n_in, D, mix, n_out=1, modi=0.0, lo=-1.0, hi=1.0, dist="uniform", ld=None):
+    pt = synth.trees(seed, 0, P, L, synth.MIXES[mix] if isinstance(mix, str) else mix, n_in, n_out, modi)
+    X = synth.dataset_X(seed, 0, D, n_in, dist, lo, hi)
+    y = synth.pagie_y(X)
+    return pt, X, y
+
+
+def to_device(pt, L, n_in, n_out=1, ld=None):
+    evogp = _evogp()
+    t, v, s = evogp.tensorize(pt.offsets, pt.types, pt.values, L, n_in, n_out)
+    if ld is not None and ld != L:
+        P = t.shape[0]
+        tt = np.full((P, ld), -1, np.int16)
+        vv = np.full((P, ld), np.nan, np.float32)
+        ss = np.zeros((P, ld), np.int16)
+        tt[:, :L], vv[:, :L], ss[:, :L] = t, v, s
+        t, v, s = tt, vv, ss
+    dev = torch.device("cuda:0")
+    return (torch.from_numpy(t).to(dev), torch.from_numpy(v).to(dev), torch.from_numpy(s).to(dev))
+
+
+def oracle_arrays(pt, L, n_in, n_out=1):
+    return oracle.tensorize(pt.offsets, pt.types, pt.values, L, n_in, n_out)
+
+
+def same_bits_mod_zero(g, r):
+    """g float32 GPU, r float64 FP32-faithful oracle: identical bits modulo +-0, NaN by class."""
+    r32 = r.astype(np.float32)
+    both_nan = np.isnan(g) & np.isnan(r32)
+    eq = (g == r32) | both_nan  # +0 == -0 compares equal
+    return eq & (np.isnan(g) == np.isnan(r32))
+
+
+def gpu_eval(dev_trees, X, n_out, strategy, L=None, ld=None, x_layout="rowmajor"):
+    evogp = _evogp()
+    t, v, s = dev_trees
+    Xd = torch.from_numpy(np.ascontiguousarray(X if x_layout == "rowmajor" else X.T)).cuda()
+    out = evogp.eval(t, v, s, Xd, n_outputs=n_out, strategy=strategy, x_layout=x_layout, max_len=L)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def gpu_mse(dev_trees, X, y, strategy, L=None):
+    evogp = _evogp()
+    t, v, s = dev_trees
+    m = evogp.sr_fitness(t, v, s, torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(), strategy=strategy,
+                         max_len=L)
+    torch.cuda.synchronize()
+    return m.cpu().numpy()
+
+
+# ---------------------------------------------------------------- Tier A
+TIER_A_SHAPES = [
+    # (P, L, n_in, D)  — C1 exactly; reduced C2/C4 spanning several chunks + ragged tails
+    (64, 15, 2, 32),
+    (300, 63, 4, 1024),
+    (257, 63, 4, 1000),
+    (200, 127, 8, 256),
+    (33, 31, 3, 77),
+    (5, 127, 8, 20_001),
+]
+
+
+@pytest.mark.parametrize("shape", TIER_A_SHAPES)
+@pytest.mark.parametrize("strategy", ["inter", "intra"])
+def test_tier_a_ieee_bitexact(shape, strategy):
+    P, L, n_in, D = shape
+    pt, X, y = make_case(100 + P, P, L, n_in, D, "ieee", lo=-2.0, hi=2.0)
+    dt = to_device(pt, L, n_in)
+    g = gpu_eval(dt, X, 1, strategy)[:, :, 0]
+    t, v, s = oracle_arrays(pt, L, n_in)
+    r32 = oracle.evaluate(t, v, s, X, mode=1)[:, :, 0]
+    ok = same_bits_mod_zero(g, r32)
+    assert ok.all(), f"{(~ok).sum()} mismatches, first {np.argwhere(~ok)[:3]}"
+    # literal north-star tolerance vs FP64 (identical NaN/Inf class)
+    r64, e, rob = oracle.evaluate(t, v, s, X, mode=0, certify=True)
+    lit = oracle.within_tol(g, r64[:, :, 0])
+    cert = oracle.certified_points(r64[:, :, 0], e[:, :, 0], rob[:, :, 0])
+    assert lit[cert].all()
+    assert lit.mean() >= 0.999, lit.mean()
+    # MSE vs FP64 oracle
+    m = gpu_mse(dt, X, y, strategy)
+    m64 = oracle.mse(r64[:, :, 0], y)
+    fin = np.isfinite(m64)
+    assert (np.isfinite(m) == fin).all()
+    rel = np.abs(m[fin] - m64[fin]) / np.maximum(np.abs(m64[fin]), 1e-300)
+    assert (rel <= TOL).mean() >= 0.99, np.sort(rel)[-5:]
+    mcert = oracle.mse_certified_trees(r64[:, :, 0], e[:, :, 0], rob[:, :, 0], y)
+    assert (rel[mcert[fin]] <= TOL).all()
+
+
+# ---------------------------------------------------------------- Tier B
+@pytest.mark.parametrize("mix", ["paper", "bounded", "full"])
+@pytest.mark.parametrize("strategy", ["inter", "intra"])
+def test_tier_b_certified(mix, strategy):
+    P, L, n_in, D = 400, 63, 4, 1024
+    pt, X, y = make_case(200, P, L, n_in, D, mix)
+    dt = to_device(pt, L, n_in)
+    g = gpu_eval(dt, X, 1, strategy)[:, :, 0]
+    t, v, s = oracle_arrays(pt, L, n_in)
+    r64, e, rob = oracle.evaluate(t, v, s, X, mode=0, certify=True)
+    r64, e, rob = r64[:, :, 0], e[:, :, 0], rob[:, :, 0]
+    cert = oracle.certified_points(r64, e, rob)
+    lit = oracle.within_tol(g, r64)
+    assert lit[cert].all(), f"{(~lit & cert).sum()} certified points outside tolerance"
+    # literal pass rate is reported; a large shortfall vs SURVEY C5 means a bug
+    floor = {"paper": 0.85, "bounded": 0.98, "full": 0.90}[mix]
+    assert lit.mean() >= floor, (mix, lit.mean(), cert.mean())
+    m = gpu_mse(dt, X, y, strategy)
+    m64 = oracle.mse(r64, y)
+    mc = oracle.mse_certified_trees(r64, e, rob, y)
+    rel = np.abs(m[mc] - m64[mc]) / np.abs(m64[mc])
+    assert (rel <= TOL).all()
+
+
+# ---------------------------------------------------------------- Tier C / D
+@pytest.mark.parametrize("mix", ["paper", "full"])
+def test_tier_c_fused_reduction(mix):
+    P, L, n_in, D = 500, 63, 4, 3000
+    pt, X, y = make_case(300, P, L, n_in, D, mix)
+    dt = to_device(pt, L, n_in)
+    for strategy in ("inter", "intra"):
+        g = gpu_eval(dt, X, 1, strategy)[:, :, 0].astype(np.float64)
+        ref = oracle.mse(g, y)  # FP64 recompute from the GPU's own outputs
+        m = gpu_mse(dt, X, y, strategy)
+        fin = np.isfinite(ref)
+        assert (np.isnan(m) == np.isnan(ref)).all()
+        assert (np.isinf(m) == np.isinf(ref)).all()
+        rel = np.abs(m[fin] - ref[fin]) / np.maximum(np.abs(ref[fin]), 1e-300)
+        assert rel.max() <= 1e-9, rel.max()
+
+
+@pytest.mark.parametrize("mix,n_out,modi,n_in", [("full", 1, 0.0, 4), ("paper", 1, 0.0, 8), ("full", 6, 0.1, 17)])
+def test_tier_d_kernels_bit_identical(mix, n_out, modi, n_in):
+    P, L, D = 300, 63, 5000
+    pt, X, y = make_case(400, P, L, n_in, D, mix, n_out=n_out, modi=modi)
+    dt = to_device(pt, L, n_in, n_out)
+    a = gpu_eval(dt, X, n_out, "inter")
+    b = gpu_eval(dt, X, n_out, "intra")
+    assert a.tobytes() == b.tobytes() or np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    if n_out == 1:
+        ma, mb = gpu_mse(dt, X, y, "inter"), gpu_mse(dt, X, y, "intra")
+        fin = np.isfinite(ma)
+        assert (np.isfinite(mb) == fin).all()
+        assert np.allclose(ma[fin], mb[fin], rtol=1e-12, atol=0)
+
+
+def test_determinism():
+    pt, X, y = make_case(500, 500, 63, 4, 4096, "paper")
+    dt = to_device(pt, 63, 4)
+    for strategy in ("inter", "intra"):
+        a = gpu_mse(dt, X, y, strategy)
+        b = gpu_mse(dt, X, y, strategy)
+        assert a.tobytes() == b.tobytes()
+
+
+# ---------------------------------------------------------------- multi-output (Modi)
+def test_fig6_on_gpu():
+    import json
+    import os
+
+    from tests.conftest import GOLDEN
+
+    g = json.load(open(os.path.join(GOLDEN, "fig6_modi_tree.json")))
+    pt = synth.PrefixTrees(np.array([0, 13], np.int64), np.array(g["types"], np.int16),
+                           np.array(g["values"], np.float32))
+    dt = to_device(pt, 13, 5, 3)
+    X = np.array([[g["inputs"][k] for k in "abcde"]], np.float32)
+    for strategy in ("inter", "intra"):
+        out = gpu_eval(dt, X, 3, strategy)[0, 0]
+        np.testing.assert_array_equal(out, np.array(g["expected_outputs"], np.float32))
+
+
+@pytest.mark.parametrize("strategy", ["inter", "intra"])
+def test_multi_output_ieee_bitexact(strategy):
+    P, L, n_in, n_out, D = 200, 63, 17, 6, 4096
+    pt, X, _ = make_case(600, P, L, n_in, D, "ieee", n_out=n_out, modi=0.1, dist="normal")
+    dt = to_device(pt, L, n_in, n_out)
+    g = gpu_eval(dt, X, n_out, strategy)
+    t, v, s = oracle_arrays(pt, L, n_in, n_out)
+    r32 = oracle.evaluate(t, v, s, X, n_out=n_out, mode=1)
+    ok = same_bits_mod_zero(g, r32)
+    assert ok.all(), (~ok).sum()
+    nz = (r32 != 0).any(axis=1).mean()
+    assert nz > 0.3  # some slots are written by Modi nodes (reading R4)
+
+
+@pytest.mark.parametrize("strategy", ["inter", "intra"])
+def test_multi_output_full_certified(strategy):
+    P, L, n_in, n_out, D = 200, 63, 17, 6, 2048
+    pt, X, _ = make_case(700, P, L, n_in, D, "full", n_out=n_out, modi=0.1, dist="normal")
+    dt = to_device(pt, L, n_in, n_out)
+    g = gpu_eval(dt, X, n_out, strategy)
+    t, v, s = oracle_arrays(pt, L, n_in, n_out)
+    r64, e, rob = oracle.evaluate(t, v, s, X, n_out=n_out, mode=0, certify=True)
+    cert = oracle.certified_points(r64, e, rob)
+    lit = oracle.within_tol(g, r64)
+    assert lit[cert].all()
+    assert lit.mean() > 0.9
+
+
+# ---------------------------------------------------------------- edge cases
+def test_edge_single_tree_single_point_and_leaves():
+    pt = synth.PrefixTrees(np.array([0, 1, 2, 5], np.int64), np.array([0, 1, 3, 1, 0], np.int16),
+                           np.array([0.25, 1, 0, 0, 2.0], np.float32))
+    X = np.array([[3.0, -7.0]], np.float32)
+    dt = to_device(pt, 4, 2)
+    for strategy in ("inter", "intra"):
+        out = gpu_eval(dt, X, 1, strategy)[:, 0, 0]
+        np.testing.assert_array_equal(out, np.array([0.25, -7.0, 5.0], np.float32))
+
+
+@pytest.mark.parametrize("ld", [127, 128, 133])
+def test_edge_row_stride_and_soa(ld):
+    P, L, n_in, D = 70, 127, 8, 700
+    pt, X, y = make_case(800, P, L, n_in, D, "ieee")
+    dt = to_device(pt, L, n_in, ld=ld)
+    t, v, s = oracle_arrays(pt, L, n_in)
+    r32 = oracle.evaluate(t, v, s, X, mode=1)[:, :, 0]
+    for strategy in ("inter", "intra"):
+        for lay in ("rowmajor", "soa"):
+            g = gpu_eval(dt, X, 1, strategy, L=L, x_layout=lay)[:, :, 0]
+            assert same_bits_mod_zero(g, r32).all(), (strategy, lay)
+
+
+def test_edge_deep_stack_spill():
+    """Left-comb trees have stack depth = #leaves (64 at L=127): exercises the
+    global spill area beyond the shared-memory slots."""
+    L, n_in = 127, 2
+    rng = np.random.default_rng(5)
+    offs, tys, vas = [0], [], []
+    for p in range(40):
+        nf = 63
+        ty = [3] * nf + [1] * (nf + 1)
+        va = list(rng.choice([0, 1, 2, 3], size=nf).astype(np.float32)) + list(rng.integers(0, 2, nf + 1))
+        tys += ty
+        vas += va
+        offs.append(len(tys))
+    pt = synth.PrefixTrees(np.array(offs, np.int64), np.array(tys, np.int16), np.array(vas, np.float32))
+    X = synth.dataset_X(9, 0, 600, n_in, lo=0.5, hi=1.5)
+    dt = to_device(pt, L, n_in)
+    t, v, s = oracle_arrays(pt, L, n_in)
+    r32 = oracle.evaluate(t, v, s, X, mode=1)[:, :, 0]
+    for strategy in ("inter", "intra"):
+        g = gpu_eval(dt, X, 1, strategy)[:, :, 0]
+        assert same_bits_mod_zero(g, r32).all(), strategy
+
+
+def test_edge_malformed_row_nan_and_flag():
+    evogp = _evogp()
+    pt, X, y = make_case(900, 20, 15, 2, 64, "paper")
+    t, v, s = evogp.tensorize(pt.offsets, pt.types, pt.values, 15, 2)
+    t = t.copy()
+    t[3, 0] = 1  # root becomes a VAR: leftover operands (malformed)
+    v = v.copy()
+    v[3, 0] = 0
+    t[7, 1] = 5  # invalid kind
+    dev = [torch.from_numpy(a).cuda() for a in (t, v, s)]
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    for strategy in ("inter", "intra"):
+        ws = evogp.Workspace(20, 64, 15, 2, 1, device="cuda:0")
+        out = evogp.eval(*dev, Xd, strategy=strategy, workspace=ws)
+        m = evogp.sr_fitness(*dev, Xd, yd, strategy=strategy, workspace=ws)
+        torch.cuda.synchronize()
+        o = out.cpu().numpy()
+        assert np.isnan(o[3]).all() and np.isnan(o[7]).all()
+        assert not np.isnan(o[[0, 1, 2, 4, 5, 6]]).any()
+        mm = m.cpu().numpy()
+        assert np.isnan(mm[3]) and np.isnan(mm[7])
+        assert evogp.check_device_flags(ws) & 1
+        assert evogp.check_device_flags(ws) == 0
+
+
+def test_data_shard_algebra_single_gpu():
+    """sum over row-shards of evogp_sr_sse == full SSE (FP64 re-association
+    only), i.e. the datapoint-sharded multi-GPU algebra, on one GPU."""
+    evogp = _evogp()
+    P, L, n_in, D = 100, 127, 8, 40_000
+    pt, X, y = make_case(1000, P, L, n_in, D, "paper")
+    t, v, s = to_device(pt, L, n_in)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    full = evogp.sr_sse(t, v, s, Xd, yd)
+    parts = [evogp.sr_sse(t, v, s, Xd[a:b].contiguous(), yd[a:b].contiguous())
+             for a, b in [(0, 13_000), (13_000, 26_001), (26_001, D)]]
+    tot = sum(parts)
+    torch.cuda.synchronize()
+    f, g = full.cpu().numpy(), tot.cpu().numpy()
+    fin = np.isfinite(f)
+    assert (np.isfinite(g) == fin).all()
+    assert np.allclose(f[fin], g[fin], rtol=1e-12, atol=0)
+    mse = evogp.sr_fitness(t, v, s, Xd, yd).cpu().numpy()
+    assert np.allclose(mse[fin], f[fin] / D, rtol=1e-15)
+
+
+def test_empty_population():
+    evogp = _evogp()
+    z16 = torch.zeros((0, 15), dtype=torch.int16, device="cuda")
+    zf = torch.zeros((0, 15), dtype=torch.float32, device="cuda")
+    X = torch.zeros((10, 2), device="cuda")
+    out = evogp.eval(z16, zf, z16, X)
+    assert out.shape == (0, 10, 1)
+
+
+# ---------------------------------------------------------------- full BASELINE sizes (sampled)
+def _sample_rows(P, n, seed=0):
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(P, size=min(n, P), replace=False))
+
+
+@pytest.mark.parametrize("cfg_key,n_rows", [("c2", 10_000), ("c4", 1500), ("c5", 200)])
+def test_full_size_sampled(cfg_key, n_rows):
+    """The bench's launch configuration (strategy auto) at BASELINE.json's full
+    sizes; the oracle checks a sample of rows (all rows for C2)."""
+    evogp = _evogp()
+    cfg = synth.CONFIGS[cfg_key]
+    mix = synth.M_FULL if cfg.n_out > 1 else synth.M_PAPER
+    pt = synth.config_trees(cfg, mix)
+    X, y = synth.config_data(cfg)
+    t, v, s = to_device(pt, cfg.max_len, cfg.n_in, cfg.n_out)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    rows = _sample_rows(cfg.P, n_rows)
+    sub = synth.PrefixTrees(*_subset(pt, rows))
+    ot, ov, osz = oracle_arrays(sub, cfg.max_len, cfg.n_in, cfg.n_out)
+    if cfg.n_out == 1:
+        m = evogp.sr_fitness(t, v, s, Xd, yd).cpu().numpy()[rows]
+        r64, e, rob = oracle.evaluate(ot, ov, osz, X, mode=0, certify=True)
+        m64 = oracle.mse(r64[:, :, 0], y)
+        mc = oracle.mse_certified_trees(r64[:, :, 0], e[:, :, 0], rob[:, :, 0], y)
+        rel = np.abs(m[mc] - m64[mc]) / np.abs(m64[mc])
+        assert (rel <= TOL).all()
+        assert mc.sum() >= 1
+        # literal MSE pass rate (reported; SURVEY C5 measured ~57% of paper-mix trees)
+        fin = np.isfinite(m64) & np.isfinite(m)
+        lit = np.abs(m[fin] - m64[fin]) <= TOL * np.abs(m64[fin])
+        assert lit.mean() > 0.3
+    else:
+        out = evogp.eval(t, v, s, Xd, n_outputs=cfg.n_out)
+        g = out[torch.from_numpy(rows).cuda()].cpu().numpy()
+        r64, e, rob = oracle.evaluate(ot, ov, osz, X, n_out=cfg.n_out, mode=0, certify=True)
+        cert = oracle.certified_points(r64, e, rob)
+        lit = oracle.within_tol(g, r64)
+        assert lit[cert].all()
+
+
+def _subset(pt, rows):
+    offs, tys, vas = [0], [], []
+    for r in rows:
+        a, b = pt.tree(int(r))
+        tys.append(a)
+        vas.append(b)
+        offs.append(offs[-1] + len(a))
+    return np.array(offs, np.int64), np.concatenate(tys), np.concatenate(vas)
+
+
+def test_full_size_c3_sampled_trees():
+    """C3 (P=1000, L=127, D=2^20, kernel (b)): MSE of sampled trees vs oracle."""
+    evogp = _evogp()
+    cfg = synth.CONFIGS["c3"]
+    pt = synth.config_trees(cfg, synth.M_PAPER)
+    X, y = synth.config_data(cfg)
+    t, v, s = to_device(pt, cfg.max_len, cfg.n_in)
+    m = evogp.sr_fitness(t, v, s, torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()).cpu().numpy()
+    assert evogp.select_strategy(cfg.P, cfg.D, cfg.max_len) == "intra"
+    rows = _sample_rows(cfg.P, 16, seed=3)
+    sub = synth.PrefixTrees(*_subset(pt, rows))
+    ot, ov, osz = oracle_arrays(sub, cfg.max_len, cfg.n_in)
+    r64 = oracle.evaluate(ot, ov, osz, X, mode=0)[:, :, 0]
+    m64 = oracle.mse(r64, y)
+    fin = np.isfinite(m64)
+    assert (np.isfinite(m[rows]) == fin).all()
+    rel = np.abs(m[rows][fin] - m64[fin]) / np.abs(m64[fin])
+    # literal MSE pass rate at C3 (uncertified trees may legitimately differ)
+    assert (rel <= TOL).mean() >= 0.25, rel
