@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""bench.py — GPops/s of the EvoGP hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--mix paper]
+    python bench.py --impl reference ...        # the oracle on the host cores
+
+A step is one pass of the whole hot path over one batch: dataset staging
+(a2), strategy selection (a3), tree staging (a4), stack interpretation (a5),
+the fused FP64 SSE/MSE (a7) — or the multi-output store (a6) for c5 — and,
+for N > 1, the NCCL combine (a8). GPops/s = sum_p len_p * D / t (PAPER.md
+P:600-605 with the factor D the tables need, reading R10). Tensorizing
+(a1) is timed in the `e2e` leg only (host prefix lists -> public API ->
+host result), together with the host<->device copies.
+
+Timing: W warm-up steps, then K steps each bracketed by CUDA events on the
+launching stream; L2 is flushed (256 MiB write) before every timed step,
+outside the events; the K-step region is bracketed by barrier + synchronize;
+the reported time is the max over ranks. For N > 1 launch with torchrun.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402  (seeded inputs; no method arithmetic)
+
+METRIC = "GPops/s (nodes × datapoints / s) at 1/2/4/8 B200, % of FP32/SFU roofline"
+UNIT = "GPops/s"
+SFU_FUNCS = (3, 4, 5, 6, 9, 10, 11, 12, 15, 16)  # DIV SIN COS TAN POW LOG EXP TANH SQRT INV (R3)
+SMS = 148
+FP32_LANES = 128  # per SM per clock
+SFU_LANES = 16  # per SM per clock (measured 15.9, profiles/microbench_pipes_r01.json)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(synth.CONFIGS), default="c2")
+    ap.add_argument("--mix", choices=sorted(synth.MIXES), default=None)
+    ap.add_argument("--strategy", choices=["auto", "inter", "intra"], default="auto")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sustain-seconds", type=float, default=1.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"sm_max_mhz": 1965.0, "hbm_gbs": 6650.0}, "fallback"
+
+
+def default_mix(cfg):
+    return "full" if cfg.n_out > 1 else "paper"
+
+
+def workload_desc(cfg, mix):
+    return (f"{cfg.name}: P={cfg.P} trees, max_len={cfg.max_len}, n_inputs={cfg.n_in}, n_outputs={cfg.n_out}, "
+            f"D={cfg.D}, mix={mix}")
+
+
+def tree_stats(pt):
+    lens = np.diff(pt.offsets)
+    kinds = pt.types & 7
+    fn = kinds >= 2
+    sfu = np.isin(pt.values[fn].astype(np.int64), SFU_FUNCS).sum()
+    return int(lens.sum()), float(sfu) / max(1, len(pt.types))
+
+
+def local_shards(cfg, rank, world):
+    """c3: datapoint-sharded (strong scaling: fixed total D); others:
+    population-sharded with P trees per rank (weak scaling)."""
+    if cfg.index == 3:
+        from paper_2501_17168_b200.dist import shard_rows
+
+        d0, d1 = shard_rows(cfg.D, world, rank)
+        return "data", (0, cfg.P), (d0, d1)
+    return "pop", (rank * cfg.P, (rank + 1) * cfg.P), (0, cfg.D)
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.idx), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        sm = []
+        reasons = set()
+        smax = None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        loaded = [x for x in sm if x > 600] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- oracle (cpu_baseline / reference arm)
+def oracle_pass(pt, cfg, X, y, threads):
+    import oracle
+
+    t, v, s = oracle.tensorize(pt.offsets, pt.types, pt.values, cfg.max_len, cfg.n_in, cfg.n_out)
+    out = oracle.evaluate(t, v, s, X, n_out=cfg.n_out, mode=0, threads=threads)
+    if cfg.n_out == 1:
+        oracle.mse(out[:, :, 0], y)
+
+
+def oracle_sample(cfg, mix, target_work=4e8):
+    """A bounded sample of the workload: the first n trees (all trees if small)
+    and at most 2^16 datapoints, about `target_work` node x datapoint steps."""
+    D = min(cfg.D, 1 << 16)
+    per_tree = 0.75 * cfg.max_len * D
+    n = int(max(1, min(cfg.P, target_work // per_tree)))
+    pt = synth.trees(cfg.seed, 0, n, cfg.max_len, synth.MIXES[mix], cfg.n_in, cfg.n_out, cfg.modi_prob)
+    X, y = synth.config_data(cfg, 0, D)
+    nodes = int(np.diff(pt.offsets).sum())
+    desc = f"first {n} of {cfg.P} trees x first {D} of {cfg.D} datapoints ({nodes * D:.3e} node*dp per pass)"
+    return pt, X, y, nodes * D, desc
+
+
+def time_oracle(cfg, mix, seconds, threads):
+    pt, X, y, work, desc = oracle_sample(cfg, mix)
+    oracle_pass(pt, cfg, X, y, threads)  # warm (builds/loads the library)
+    t0 = time.perf_counter()
+    passes = 0
+    while True:
+        oracle_pass(pt, cfg, X, y, threads)
+        passes += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or passes >= 1000:
+            break
+    return work * passes / el, desc + f", {passes} passes in {el:.1f} s"
+
+
+def run_reference(args, cfg, mix):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    pt, X, y, work, desc = oracle_sample(cfg, mix)
+    for _ in range(args.warmup):
+        oracle_pass(pt, cfg, X, y, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_pass(pt, cfg, X, y, threads)
+    el = time.perf_counter() - t0
+    value = work * args.steps / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "weak" if cfg.index != 3 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_desc(cfg, mix), "parallelism": "host threads (oracle)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": "each step: " + desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    cfg = synth.CONFIGS[args.config]
+    mix = args.mix or default_mix(cfg)
+    if args.impl == "reference":
+        return run_reference(args, cfg, mix)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_17168_b200 as evogp
+    from paper_2501_17168_b200 import dist as edist
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+
+    axis, (p0, p1), (d0, d1) = local_shards(cfg, rank, world)
+    pt = synth.trees(cfg.seed, p0, p1 - p0, cfg.max_len, synth.MIXES[mix], cfg.n_in, cfg.n_out, cfg.modi_prob)
+    X, y = synth.config_data(cfg, d0, d1 - d0)
+    nodes, sfu_frac = tree_stats(pt)
+    t, v, s = evogp.tensorize(pt.offsets, pt.types, pt.values, cfg.max_len, cfg.n_in, cfg.n_out)
+    td, vd, sd = (torch.from_numpy(a).to(dev) for a in (t, v, s))
+    Xd, yd = torch.from_numpy(X).to(dev), torch.from_numpy(y).to(dev)
+    P_local, D_local = p1 - p0, d1 - d0
+    strategy = args.strategy
+    chosen = evogp.select_strategy(P_local, D_local, cfg.max_len, cfg.n_out, local) if strategy == "auto" else strategy
+    ws = evogp.Workspace(P_local, D_local, cfg.max_len, cfg.n_in, cfg.n_out, device=dev)
+    out_eval = torch.empty((P_local, D_local, cfg.n_out), dtype=torch.float32, device=dev) if cfg.n_out > 1 else None
+    mse_local = torch.full((P_local,), float("nan"), dtype=torch.float64, device=dev)
+    P_total = cfg.P * world if axis == "pop" else cfg.P
+
+    def step():
+        if cfg.n_out > 1:
+            evogp.eval(td, vd, sd, Xd, n_outputs=cfg.n_out, strategy=strategy, out=out_eval, workspace=ws)
+            return out_eval
+        if axis == "data":
+            if world == 1:
+                return evogp.sr_fitness(td, vd, sd, Xd, yd, strategy=strategy, out=mse_local, workspace=ws)
+            return edist.sr_fitness_data_sharded(
+                td, vd, sd, Xd, yd, cfg.D, out=mse_local,
+                sse_fn=lambda a, b, c, x, yy, o: evogp.sr_sse(a, b, c, x, yy, strategy=strategy, out=o, workspace=ws))
+        if world == 1:
+            return evogp.sr_fitness(td, vd, sd, Xd, yd, strategy=strategy, out=mse_local, workspace=ws)
+        return edist.sr_fitness_population_sharded(
+            td, vd, sd, Xd, yd, P_total, local_out=mse_local,
+            fitness_fn=lambda a, b, c, x, yy, o: evogp.sr_fitness(a, b, c, x, yy, strategy=strategy, out=o,
+                                                                  workspace=ws))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sampler = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local])
+                           if "CUDA_VISIBLE_DEVICES" in os.environ else local)
+    sampler.start()
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    # sustain the load for the clock sampler (untimed)
+    t_end = time.perf_counter() + args.sustain_seconds
+    while time.perf_counter() < t_end:
+        for _ in range(20):
+            step()
+        torch.cuda.synchronize()
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a, b in kev:  # materialise the CUDA events before handing them to the library
+        a.record()
+        b.record()
+    launches = 0
+    barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        evogp.set_kernel_timing(*kev[i])
+        ev[i][0].record()
+        step()
+        ev[i][1].record()
+        evogp.set_kernel_timing(None, None)
+        launches += evogp.last_launch_count()
+    barrier()
+    clocks = sampler.stop()
+    step_ms = sum(a.elapsed_time(b) for a, b in ev)
+    kern_ms = sum(a.elapsed_time(b) for a, b in kev)
+    tt = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device=dev)
+    work = torch.tensor([float(nodes) * D_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(work, op=dist.ReduceOp.SUM)
+    step_ms, kern_ms = tt.tolist()
+    total_work = work.item()  # node x datapoint evaluations per step, all ranks
+    value = total_work * args.steps / (step_ms * 1e-3)
+
+    # ---- e2e: host prefix lists -> tensorize -> H2D -> device call -> D2H
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
+        h_t, h_v, h_s = pin(np.empty_like(t)), pin(np.empty_like(v)), pin(np.empty_like(s))
+        h_X, h_y = pin(X), pin(y)
+        res_len = P_total if (cfg.n_out == 1) else P_local * D_local * cfg.n_out
+        h_res = torch.empty(res_len, dtype=torch.float64 if cfg.n_out == 1 else torch.float32).pin_memory()
+        h2d = sum(x.numel() * x.element_size() for x in (h_t, h_v, h_s, h_X, h_y))
+        d2h = h_res.numel() * h_res.element_size()
+
+        def e2e_step():
+            evogp.tensorize(pt.offsets, pt.types, pt.values, cfg.max_len, cfg.n_in, cfg.n_out,
+                            out=(h_t.numpy(), h_v.numpy(), h_s.numpy()))
+            for dst, src in ((td, h_t), (vd, h_v), (sd, h_s), (Xd, h_X), (yd, h_y)):
+                dst.copy_(src, non_blocking=True)
+            r = step()
+            h_res.copy_(r.reshape(-1), non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        barrier()
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e2e = {"value": total_work * args.steps / el.item(), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "includes": "host tensorize (a1) + H2D + hot path + D2H"}
+
+    if rank == 0:
+        peaks, peak_src = measured_peaks()
+        f = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        r_fp32 = SMS * FP32_LANES * f
+        r_sfu = SMS * SFU_LANES * f
+        roof = 1.0 / max(1.0 / r_fp32, sfu_frac / r_sfu)  # per GPU
+        per_launch_work = float(nodes) * D_local  # rank 0's units per launch
+        achieved = per_launch_work * args.steps / (kern_ms * 1e-3)
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_{chosen}_summary.json")
+        if os.path.exists(prof):
+            with open(prof) as fh:
+                traffic = json.load(fh).get("dram_bytes_per_launch")
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if axis == "data" else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": workload_desc(cfg, mix), "P_per_rank": P_local, "D_per_rank": D_local,
+                       "max_len": cfg.max_len, "n_inputs": cfg.n_in, "n_outputs": cfg.n_out,
+                       "mean_len": nodes / max(1, P_local), "sfu_node_fraction": sfu_frac,
+                       "strategy": chosen, "parallelism": f"{axis}-shard x{world}",
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "step": ("evogp_eval" if cfg.n_out > 1 else "evogp_sr_fitness") +
+                               (" + NCCL combine" if world > 1 else "")},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": roof, "unit": UNIT, "frac": achieved / roof,
+                         "traffic": traffic, "kernel": f"k_{chosen}",
+                         "peak_basis": f"{SMS} SMs x min({FP32_LANES} FP32, {SFU_LANES}/s MUFU) lanes/clk at "
+                                       f"sm_max_mhz={f / 1e6:.0f} ({peak_src}), s={sfu_frac:.3f}"},
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "e2e": e2e,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            cv, desc = time_oracle(cfg, mix, args.cpu_seconds, threads)
+            line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

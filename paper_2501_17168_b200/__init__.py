@@ -23,7 +23,7 @@ _LIB = _lib.load()
 
 __all__ = [
     "tensorize", "eval", "sr_fitness", "sr_sse", "select_strategy", "workspace_size", "Workspace",
-    "check_device_flags", "EvogpError", "last_launch_count", "STRATEGIES",
+    "check_device_flags", "EvogpError", "last_launch_count", "set_kernel_timing", "STRATEGIES",
 ]
 
 STRATEGIES = {"auto": STRATEGY_AUTO, "inter": STRATEGY_INTER, "intra": STRATEGY_INTRA,
@@ -46,15 +46,22 @@ def _vp(a) -> ctypes.c_void_p:
     return ctypes.c_void_p(a.data_ptr())
 
 
-def tensorize(offsets, types, values, max_len: int, n_inputs: int, n_outputs: int = 1):
-    """Host: prefix CSR lists -> (type[P,L] int16, value[P,L] float32, size[P,L] int16)."""
+def tensorize(offsets, types, values, max_len: int, n_inputs: int, n_outputs: int = 1, out=None):
+    """Host: prefix CSR lists -> (type[P,L] int16, value[P,L] float32, size[P,L] int16).
+    ``out`` may supply the three host arrays (e.g. numpy views of pinned memory)."""
     offsets = np.ascontiguousarray(offsets, dtype=np.int64)
     types = np.ascontiguousarray(types, dtype=np.int16)
     values = np.ascontiguousarray(values, dtype=np.float32)
     P = len(offsets) - 1
-    ot = np.empty((P, max_len), dtype=np.int16)
-    ov = np.empty((P, max_len), dtype=np.float32)
-    osz = np.empty((P, max_len), dtype=np.int16)
+    if out is not None:
+        ot, ov, osz = out
+        for a, dt in zip(out, (np.int16, np.float32, np.int16)):
+            if a.dtype != dt or a.shape != (P, max_len) or not a.flags.c_contiguous:
+                raise ValueError("tensorize out arrays must be C-contiguous (P, max_len) int16/float32/int16")
+    else:
+        ot = np.empty((P, max_len), dtype=np.int16)
+        ov = np.empty((P, max_len), dtype=np.float32)
+        osz = np.empty((P, max_len), dtype=np.int16)
     et = np.zeros(1, dtype=np.int64)
     en = np.zeros(1, dtype=np.int32)
     if types.size == 0:
@@ -193,3 +200,13 @@ def check_device_flags(workspace: Workspace, stream=None) -> int:
 
 def last_launch_count() -> int:
     return int(_LIB.evogp_last_launch_count())
+
+
+def set_kernel_timing(start_event=None, end_event=None) -> None:
+    """Bracket the dominant kernel of subsequent device calls (this thread)
+    with two torch.cuda.Event(enable_timing=True) events; None disables."""
+    a = ctypes.c_void_p(start_event.cuda_event) if start_event is not None else ctypes.c_void_p(0)
+    b = ctypes.c_void_p(end_event.cuda_event) if end_event is not None else ctypes.c_void_p(0)
+    st = _LIB.evogp_set_kernel_timing(a, b)
+    if st != OK:
+        raise EvogpError(st, "evogp_set_kernel_timing")

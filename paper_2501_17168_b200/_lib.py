@@ -22,7 +22,7 @@ X_ROWMAJOR, X_SOA = 0, 1
 EXPORTS = (
     "evogp_tensorize", "evogp_workspace_size", "evogp_eval", "evogp_sr_fitness", "evogp_sr_sse",
     "evogp_select_strategy", "evogp_check_device_flags", "evogp_status_string", "evogp_last_error",
-    "evogp_last_launch_count",
+    "evogp_last_launch_count", "evogp_set_kernel_timing",
 )
 
 
@@ -54,4 +54,6 @@ def load() -> ctypes.CDLL:
     lib.evogp_last_error.restype = ctypes.c_char_p
     lib.evogp_last_launch_count.argtypes = []
     lib.evogp_last_launch_count.restype = ctypes.c_int32
+    lib.evogp_set_kernel_timing.argtypes = [vp, vp]
+    lib.evogp_set_kernel_timing.restype = ctypes.c_int
     return lib

@@ -13,6 +13,8 @@ namespace evogp {
 namespace {
 thread_local char t_last_error[512] = "no error";
 thread_local int32_t t_last_launches = 0;
+thread_local void* t_ev_start = nullptr;
+thread_local void* t_ev_end = nullptr;
 
 int current_device() {
   int dev = 0;
@@ -69,17 +71,17 @@ int run(int mode, const int16_t* type, const float* value, const int16_t* size, 
   kp.size = size;
   kp.ld = ld;
   kp.xs = reinterpret_cast<const float*>(ws + pl.off_xs);
-  kp.y = y;
   kp.out = out;
   kp.res = res;
   kp.div_by_D = div_by_D;
-  kp.flags = reinterpret_cast<int32_t*>(ws + pl.off_flags);
+  kp.ctl = reinterpret_cast<Control*>(ws + pl.off_ctl);
   kp.counters = reinterpret_cast<int32_t*>(ws + pl.off_counters);
   kp.partials = reinterpret_cast<double*>(ws + pl.off_partials);
-  kp.spill = reinterpret_cast<float*>(ws + pl.off_spill);
+  kp.deep_locks = reinterpret_cast<int32_t*>(ws + pl.off_locks);
+  kp.deep = reinterpret_cast<float*>(ws + pl.off_deep);
   kp.use_tma = (ld % 8 == 0) && aligned(type, 16) && aligned(value, 16);
   int nl = 0;
-  st = launch(pl, mode, X, x_layout, stream, &nl);
+  st = launch(pl, mode, X, x_layout, y, stream, &nl, t_ev_start, t_ev_end);
   t_last_launches = nl;
   return st;
 }
@@ -187,3 +189,10 @@ extern "C" const char* evogp_status_string(int status) {
 extern "C" const char* evogp_last_error(void) { return t_last_error; }
 
 extern "C" int32_t evogp_last_launch_count(void) { return t_last_launches; }
+
+extern "C" int evogp_set_kernel_timing(void* start_event, void* end_event) {
+  if ((start_event == nullptr) != (end_event == nullptr)) return fail(EVOGP_E_ARG, "need both events or neither");
+  t_ev_start = start_event;
+  t_ev_end = end_event;
+  return EVOGP_OK;
+}

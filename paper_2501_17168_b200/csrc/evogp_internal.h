@@ -31,20 +31,28 @@ EVOGP_HD constexpr int func_arity(int f) {
 }
 
 // Pre-decoded node word staged in shared memory (8 bytes, one LDS.64).
-// op: 0 CONST, 1 VAR, 2 + function id.  slot: Modi output slot or 0xFF.
-// arg: VAR input index.  val: CONST literal.
-enum : uint8_t { OP_CONST = 0, OP_VAR = 1, OP_FN = 2 };
-constexpr uint8_t kNoSlot = 0xFF;
+// w0: bits 0-7 op (0 CONST, 1 VAR, 2 + function id), bits 8-15 Modi slot
+//     (0xFF: none).
+// w1: CONST: the literal's bits; VAR: the input's float offset in the staged
+//     SoA dataset (index * Dpad), so a leaf needs no multiply at run time.
+enum : uint32_t { OP_CONST = 0, OP_VAR = 1, OP_FN = 2 };
+constexpr uint32_t kNoSlot = 0xFF;
 struct alignas(8) Node {
-  uint8_t op;
-  uint8_t slot;
-  uint16_t arg;
-  float val;
+  uint32_t w0;
+  uint32_t w1;
 };
 
 enum Mode : int { MODE_EVAL1 = 0, MODE_EVALN = 1, MODE_SSE = 2 };
 
-// Everything a kernel launch needs; built by plan() on the host.
+// Layout of the small control block at the start of the workspace.
+struct Control {
+  int32_t flags;            // device flags (bit 0: malformed row evaluated as NaN)
+  int32_t pad;
+  unsigned long long work;  // dynamic work-queue ticket counter (zeroed by k_stage_x)
+  unsigned long long deep;  // deep-stack pool ticket counter
+};
+
+// Everything a kernel launch needs; built by plan_problem() on the host.
 struct KParams {
   const int16_t* type;
   const float* value;
@@ -56,8 +64,7 @@ struct KParams {
   int32_t n_out;
   int64_t D;
   int64_t Dpad;
-  const float* xs;  // staged SoA X: n_in x Dpad
-  const float* y;
+  const float* xs;  // staged SoA X: n_in rows of Dpad floats, then (SSE) one row of y
   float* out;       // eval outputs
   double* res;      // mse or sse
   int32_t div_by_D; // 1: mse, 0: sse
@@ -65,17 +72,20 @@ struct KParams {
   int32_t nparts;   // partial sums per tree (inter: nch, intra: nseg)
   int32_t nseg;     // intra: segments per tree
   int32_t seg_chunks;
-  int32_t SD;          // shared-memory stack slots per warp
-  int32_t spill_slots; // global spill slots per warp
-  int32_t tree_bytes;  // per-warp (inter) or per-CTA (intra) decoded-tree bytes
-  int32_t warp_smem_bytes;
-  int32_t raw_bytes;   // intra: raw row staging bytes (type + value), 16B multiple
-  int32_t use_tma;     // intra: rows are 16B aligned -> cp.async.bulk staging
-  int32_t out_magic;   // ceil(2^32 / n_out) for index split in the Modi store
+  int32_t SD;               // shared-memory stack slots per warp
+  int32_t tree_bytes;       // decoded-tree bytes ((L + 1) nodes, 16B multiple)
+  int32_t warp_smem_bytes;  // per-warp stack (+ Modi accumulator) bytes
+  int32_t raw_type_bytes;   // intra: raw type row bytes (16B multiple)
+  int32_t raw_value_bytes;  // intra: raw value row bytes (16B multiple)
+  int32_t use_tma;          // intra: rows are 16B aligned -> cp.async.bulk staging
+  int32_t out_magic;        // ceil(2^32 / n_out) for the index split in the Modi store
+  int32_t deep_slots;       // size of the deep-stack pool
+  int64_t deep_slot_floats; // floats per deep-stack slot (depth bound x 32K)
   double* partials;
   int32_t* counters;
-  int32_t* flags;
-  float* spill;
+  Control* ctl;
+  int32_t* deep_locks;
+  float* deep;
 };
 
 struct Plan {
@@ -86,13 +96,14 @@ struct Plan {
   size_t smem_bytes;
   KParams kp;
   // workspace layout
-  size_t off_flags, off_xs, off_counters, off_partials, off_spill, total;
+  size_t off_ctl, off_xs, off_counters, off_partials, off_locks, off_deep, total;
 };
 
 // kernels.cu
 int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_t n_out, int mode, int strategy,
                  int device);
-int launch(Plan& pl, int mode, const float* X, int32_t x_layout, void* stream, int* n_launches);
+int launch(Plan& pl, int mode, const float* X, int32_t x_layout, const float* y, void* stream, int* n_launches,
+           void* ev_start = nullptr, void* ev_end = nullptr);
 int select_strategy(int64_t P, int64_t D, int32_t L, int32_t n_out, int device);
 
 void set_last_error(const char* msg);

@@ -1,17 +1,19 @@
 // kernels.cu — sm_100a kernels of the EvoGP hot path (arXiv 2501.17168).
 //
-//   k_stage_x        a2: X (row-major or SoA) -> padded SoA Xs[n_in][Dpad];
-//                         clears the per-tree completion counters.
+//   k_stage_x        a2: X (row-major or SoA) -> padded SoA rows Xs[n_in][Dpad]
+//                         (+ y as row n_in for the SSE), clears the per-tree
+//                         completion counters and the work-queue tickets.
 //   k_inter<K,MODE>  (a) inter-individual: one warp per (tree, chunk of 32*K
-//                         datapoints); the warp stages and pre-decodes its tree
-//                         into shared memory, each lane evaluates K datapoints
-//                         (PAPER §III-C "hybrid parallelism").
+//                         datapoints) pulled from a device work queue; the warp
+//                         stages and pre-decodes its tree into shared memory,
+//                         each lane evaluates K datapoints (PAPER §III-C
+//                         "hybrid parallelism").
 //   k_intra<K,MODE>  (b) intra-individual: one CTA per (tree, datapoint range);
 //                         the tree row is staged into shared memory by a TMA
 //                         bulk copy (cp.async.bulk + mbarrier) and shared by all
 //                         8 warps, datapoints striped across the warps (PAPER
-//                         §III-C "data-level parallelism", with shared
-//                         memory in place of the paper's constant memory).
+//                         §III-C "data-level parallelism", shared memory
+//                         standing in for the paper's constant memory).
 // Both run the same per-point interpreter (stack evaluation in reverse prefix
 // order), so their outputs are bit-identical. MODE selects the epilogue:
 // single-output store, Modi multi-output store, or the fused SR
@@ -23,45 +25,47 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 
 #include "evogp_internal.h"
+#include "fastmath.cuh"
 
 namespace evogp {
 
 #define FULL_MASK 0xFFFFFFFFu
+#define FOR_K _Pragma("unroll") for (int k = 0; k < K; ++k)
+
+constexpr float kDelta = 0.001f;  // protection threshold (reading R3)
 
 // ------------------------------------------------------------------------
-// Node decode + validation (R2/R3; mirrors the tensorizer's rules)
+// Node decode + validation (R2/R3; same rules as the tensorizer)
 // ------------------------------------------------------------------------
-__device__ __forceinline__ bool decode_node(int16_t t, float v, int n_in, int n_out, Node& nd, int& ar) {
+__device__ __forceinline__ bool decode_node(int16_t t, float v, int n_in, int n_out, int64_t Dpad, Node& nd,
+                                            int& ar) {
   const unsigned tw = static_cast<uint16_t>(t);
   const unsigned kind = tw & 7u, modi = (tw >> 3) & 1u, slot = (tw >> 8) & 0xFFu;
   bool ok = (tw & 0xF0u) == 0 && kind <= 4;
-  nd.val = v;
-  nd.slot = kNoSlot;
-  nd.arg = 0;
   if (kind == 0) {
-    nd.op = OP_CONST;
+    nd.w0 = OP_CONST | (kNoSlot << 8);
+    nd.w1 = __float_as_uint(v);
     ar = 0;
     ok = ok && !modi && slot == 0;
   } else if (kind == 1) {
-    nd.op = OP_VAR;
-    ar = 0;
     const bool in_range = floorf(v) == v && v >= 0.f && v < static_cast<float>(n_in);
+    nd.w0 = OP_VAR | (kNoSlot << 8);
+    nd.w1 = in_range ? static_cast<uint32_t>(static_cast<int64_t>(v) * Dpad) : 0u;
+    ar = 0;
     ok = ok && !modi && slot == 0 && in_range;
-    nd.arg = in_range ? static_cast<uint16_t>(static_cast<int>(v)) : 0;
   } else {
     const bool known = floorf(v) == v && v >= 0.f && v < static_cast<float>(kNumFuncs);
     const int f = known ? static_cast<int>(v) : 0;
     ar = kind <= 4 ? static_cast<int>(kind) - 1 : 0;
     ok = ok && known && func_arity(f) == ar;
-    nd.op = static_cast<uint8_t>(OP_FN + f);
-    if (modi) {
-      ok = ok && n_out > 1 && static_cast<int>(slot) < n_out;
-      nd.slot = static_cast<uint8_t>(slot);
-    } else {
-      ok = ok && slot == 0;
-    }
+    if (modi) ok = ok && n_out > 1 && static_cast<int>(slot) < n_out;
+    else ok = ok && slot == 0;
+    nd.w0 = (OP_FN + f) | ((modi ? slot : kNoSlot) << 8);
+    nd.w1 = 0;
   }
   return ok;
 }
@@ -72,10 +76,11 @@ struct TreeInfo {
   bool valid;
 };
 
-// One warp stages row `tp` into s_tree (pre-decoded Node words) and validates
-// it: with c_i = 1 - arity_i, the stack size after processing node i is the
-// suffix sum d_i = sum_{j>=i} c_j; a row is well-formed iff every d_i >= 1
-// and d_0 == 1 (P:358 stack evaluation never underflows and leaves the root).
+// One warp stages row `tp` as pre-decoded Node words: node i goes to
+// s_tree[i + 1] (s_tree[0] is a pad the interpreter's prefetch may read).
+// Validation: with c_i = 1 - arity_i the stack size after processing node i
+// is the suffix sum d_i = sum_{j>=i} c_j; a row is well-formed iff every
+// d_i >= 1 and d_0 == 1 (P:358 evaluation never underflows, leaves the root).
 __device__ __forceinline__ TreeInfo stage_tree_warp(const KParams& p, int64_t tp, Node* s_tree, int lane,
                                                     const int16_t* raw_type = nullptr,
                                                     const float* raw_value = nullptr) {
@@ -94,8 +99,8 @@ __device__ __forceinline__ TreeInfo stage_tree_warp(const KParams& p, int64_t tp
       int ar;
       const int16_t t = raw_type ? trow[i] : __ldg(trow + i);
       const float v = raw_value ? vrow[i] : __ldg(vrow + i);
-      ok = decode_node(t, v, p.n_in, p.n_out, nd, ar) && ok;
-      s_tree[i] = nd;
+      ok = decode_node(t, v, p.n_in, p.n_out, p.Dpad, nd, ar) && ok;
+      s_tree[i + 1] = nd;
       c = 1 - ar;
     }
     int s = c;  // inclusive suffix scan over lanes lane..31
@@ -111,6 +116,7 @@ __device__ __forceinline__ TreeInfo stage_tree_warp(const KParams& p, int64_t tp
     }
     carry += __shfl_sync(FULL_MASK, s, 0);
   }
+  if (lane == 0) s_tree[0] = Node{OP_CONST | (kNoSlot << 8), 0u};
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     mind = min(mind, __shfl_xor_sync(FULL_MASK, mind, off));
@@ -126,10 +132,11 @@ __device__ __forceinline__ TreeInfo stage_tree_warp(const KParams& p, int64_t tp
 }
 
 // ------------------------------------------------------------------------
-// Per-lane vector of K datapoints. Points of a chunk are laid out as
+// Per-lane vectors of K datapoints. Points of a chunk are laid out as
 // [G groups][32 lanes][V] with V = min(K,4), G = K/V: lane l owns points
 // g*32*V + l*V + j, so every stack slot / X row access is one conflict-free
-// 32*V*4-byte vector access per group.
+// 32*V*4-byte vector access per group. Pointers below are lane-adjusted
+// (already offset by lane*V).
 // ------------------------------------------------------------------------
 template <int K>
 struct Lay {
@@ -139,238 +146,251 @@ struct Lay {
 };
 
 template <int K>
-__device__ __forceinline__ void vst(float* base, int lane, const float (&v)[K]) {
+__device__ __forceinline__ void vst(float* p, const float (&v)[K]) {
   constexpr int V = Lay<K>::V, G = Lay<K>::G;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     if constexpr (V == 4) {
-      reinterpret_cast<float4*>(base)[g * 32 + lane] = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+      *reinterpret_cast<float4*>(p + g * 128) = make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
     } else if constexpr (V == 2) {
-      reinterpret_cast<float2*>(base)[lane] = make_float2(v[0], v[1]);
+      *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
     } else {
-      base[lane] = v[0];
+      *p = v[0];
     }
   }
 }
 
 template <int K>
-__device__ __forceinline__ void vld(const float* base, int lane, float (&v)[K]) {
+__device__ __forceinline__ void vld(const float* p, float (&v)[K]) {
   constexpr int V = Lay<K>::V, G = Lay<K>::G;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     if constexpr (V == 4) {
-      const float4 q = reinterpret_cast<const float4*>(base)[g * 32 + lane];
+      const float4 q = *reinterpret_cast<const float4*>(p + g * 128);
       v[4 * g] = q.x;
       v[4 * g + 1] = q.y;
       v[4 * g + 2] = q.z;
       v[4 * g + 3] = q.w;
     } else if constexpr (V == 2) {
-      const float2 q = reinterpret_cast<const float2*>(base)[lane];
+      const float2 q = *reinterpret_cast<const float2*>(p);
       v[0] = q.x;
       v[1] = q.y;
     } else {
-      v[0] = base[lane];
+      v[0] = *p;
     }
   }
 }
 
 template <int K>
-__device__ __forceinline__ void vld_global_nc(const float* base, int lane, float (&v)[K]) {
+__device__ __forceinline__ void vld_nc(const float* p, float (&v)[K]) {
   constexpr int V = Lay<K>::V, G = Lay<K>::G;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     if constexpr (V == 4) {
-      const float4 q = __ldg(reinterpret_cast<const float4*>(base) + g * 32 + lane);
+      const float4 q = __ldg(reinterpret_cast<const float4*>(p + g * 128));
       v[4 * g] = q.x;
       v[4 * g + 1] = q.y;
       v[4 * g + 2] = q.z;
       v[4 * g + 3] = q.w;
     } else if constexpr (V == 2) {
-      const float2 q = __ldg(reinterpret_cast<const float2*>(base) + lane);
+      const float2 q = __ldg(reinterpret_cast<const float2*>(p));
       v[0] = q.x;
       v[1] = q.y;
     } else {
-      v[0] = __ldg(base + lane);
+      v[0] = __ldg(p);
     }
   }
 }
-
-// Operand stack: top of stack in registers, slots [0, SD) in shared memory,
-// deeper slots in a per-warp global spill area (only reached by rows deeper
-// than SD + 1; sp is warp-uniform so the branch never diverges).
-template <int K>
-struct Stack {
-  float* smem;   // SD slots of 32*K floats
-  float* spill;  // spill_slots slots of 32*K floats
-  int SD;
-  int sp;
-  int lane;
-  __device__ __forceinline__ void push(const float (&v)[K]) {
-    if (sp < SD) vst<K>(smem + sp * (32 * K), lane, v);
-    else vst<K>(spill + (sp - SD) * (32 * K), lane, v);
-    ++sp;
-  }
-  __device__ __forceinline__ void pop(float (&v)[K]) {
-    --sp;
-    if (sp < SD) vld<K>(smem + sp * (32 * K), lane, v);
-    else vld<K>(spill + (sp - SD) * (32 * K), lane, v);
-  }
-};
-
-constexpr float kDelta = 0.001f;
 
 // ------------------------------------------------------------------------
-// The interpreter: evaluate one staged tree on the lane's K datapoints of one
-// chunk (nodes from len-1 down to 0; first pop = leftmost child).
-// MULTI: Modi nodes add their value to acc[slot] and pass the rightmost
+// Heavy library functions stay out of line (one copy, called per element):
+// inlining them K times per case would blow the loop's instruction footprint
+// far past the instruction caches.
+// ------------------------------------------------------------------------
+__device__ __noinline__ float call_pow(float a, float b) { return powf(fabsf(a), b); }
+__device__ __noinline__ float call_log(float a) { return fabsf(a) > kDelta ? logf(fabsf(a)) : 0.0f; }
+__device__ __noinline__ float call_tanh(float a) { return tanhf(a); }
+
+// ------------------------------------------------------------------------
+// The interpreter: evaluate one staged tree on the lane's K datapoints of
+// one chunk (nodes from len-1 down to 0; first pop = leftmost child).
+// The top of the stack lives in registers (tos); the rest behind `stk`, a
+// lane-adjusted generic pointer into shared memory or, for rows deeper than
+// the shared slots, into a global deep-stack slot (chosen per tree, so there
+// is no per-push check and a single copy of the loop).
+// MULTI: a Modi node adds its value to acc[slot] and passes its rightmost
 // child's value to the parent (reading R4).
-// Arithmetic is FP32 with explicit round-to-nearest intrinsics (no FMA
-// contraction across nodes) and the CUDA precise math library (reading R5).
+// FP32 with explicit round-to-nearest intrinsics (no contraction across
+// nodes); IEEE-exact + - * / sqrt; fastmath.cuh sin/cos/tan; CUDA libm for
+// the others (reading R5).
 // ------------------------------------------------------------------------
 template <int K, bool MULTI>
-__device__ __forceinline__ void interpret(const Node* __restrict__ s_tree, int len, const float* __restrict__ xs,
-                                          int64_t Dpad, int64_t chunk_base, int lane, Stack<K>& st, float* acc,
-                                          float (&tos)[K]) {
-  constexpr int V = Lay<K>::V;
-  const float* xbase = xs + chunk_base;
-  auto load_leaf = [&](const Node& nd, float (&dst)[K]) {
-    if (nd.op == OP_CONST) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) dst[k] = nd.val;
-    } else {
-      vld_global_nc<K>(xbase + static_cast<int64_t>(nd.arg) * Dpad, lane, dst);
-    }
-  };
-  (void)V;
+__device__ __forceinline__ void interpret(const Node* __restrict__ tree, int len, const float* __restrict__ xl,
+                                          float* stk, float* accl, float (&tos)[K]) {
+  constexpr int SLOT = 32 * K;
+  float* top = stk;
   {
-    const Node nd = s_tree[len - 1];  // a well-formed row ends with a leaf
-    load_leaf(nd, tos);
+    const Node nd = tree[len];  // node len-1: a well-formed row ends with a leaf
+    if ((nd.w0 & 0xFFu) == OP_CONST) {
+      FOR_K tos[k] = __uint_as_float(nd.w1);
+    } else {
+      vld_nc<K>(xl + nd.w1, tos);
+    }
   }
+  uint2 nxt = *reinterpret_cast<const uint2*>(tree + len - 1);
+#pragma unroll 1
   for (int i = len - 2; i >= 0; --i) {
-    const Node nd = s_tree[i];
-    const int op = nd.op;
-    if (op <= OP_VAR) {
-      st.push(tos);
-      load_leaf(nd, tos);
+    const uint2 nd = nxt;
+    nxt = *reinterpret_cast<const uint2*>(tree + i);  // prefetch node i-1 (tree[0] is the pad)
+    const uint32_t op = nd.x & 0xFFu;
+    if (op <= OP_VAR) {  // leaf: push the old top, load the leaf
+      vst<K>(top, tos);
+      top += SLOT;
+      if (op == OP_CONST) {
+        const float v = __uint_as_float(nd.y);
+        FOR_K tos[k] = v;
+      } else {
+        vld_nc<K>(xl + nd.y, tos);
+      }
       continue;
     }
     float b[K], c[K], r[K];
-    const int f = op - OP_FN;
-    const int ar = func_arity(f);
-    if (ar >= 2) st.pop(b);
-    if (ar == 3) st.pop(c);
-    switch (f) {
-      case F_ADD:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = __fadd_rn(tos[k], b[k]);
+    // RES: where a function writes its value — straight into tos unless a
+    // Modi epilogue still needs the operands
+#define RES(k) (MULTI ? r[k] : tos[k])
+#define POP(v)   \
+  top -= SLOT;   \
+  vld<K>(top, v)
+#define BIN(F, EXPR)                     \
+  case OP_FN + F: {                      \
+    POP(b);                              \
+    FOR_K {                              \
+      const float a = tos[k], bb = b[k]; \
+      RES(k) = (EXPR);                   \
+    }                                    \
+    break;                               \
+  }
+#define UN(F, EXPR)           \
+  case OP_FN + F: {           \
+    FOR_K {                   \
+      const float a = tos[k]; \
+      RES(k) = (EXPR);        \
+    }                         \
+    break;                    \
+  }
+// trig: one range check per node (max |x| over the lane's K points); the
+// per-element slow path runs only when some point is out of the fast range
+#define TRIG(F, FAST, SLOW)                                               \
+  case OP_FN + F: {                                                       \
+    float m = 0.0f;                                                       \
+    FOR_K m = fmaxf(m, fabsf(tos[k]));                                    \
+    if (m <= kTrigReduceMax) {                                            \
+      FOR_K RES(k) = FAST(tos[k]);                                        \
+    } else {                                                              \
+      FOR_K {                                                             \
+        const float a = tos[k];                                           \
+        RES(k) = fabsf(a) <= kTrigReduceMax ? FAST(a) : SLOW(a);          \
+      }                                                                   \
+    }                                                                     \
+    break;                                                                \
+  }
+    switch (op) {
+      BIN(F_ADD, __fadd_rn(a, bb))
+      BIN(F_SUB, __fsub_rn(a, bb))
+      BIN(F_MUL, __fmul_rn(a, bb))
+      BIN(F_DIV, fabsf(bb) > kDelta ? __fdiv_rn(a, bb) : 1.0f)
+      TRIG(F_SIN, fm_sin_fast, slow_sinf)
+      TRIG(F_COS, fm_cos_fast, slow_cosf)
+      TRIG(F_TAN, fm_tan_fast, slow_tanf)
+      BIN(F_MAX, fmaxf(a, bb))
+      BIN(F_MIN, fminf(a, bb))
+      BIN(F_POW, call_pow(a, bb))
+      UN(F_LOG, call_log(a))
+      UN(F_EXP, expf(a))
+      UN(F_TANH, call_tanh(a))
+      UN(F_NEG, -a)
+      UN(F_ABS, fabsf(a))
+      UN(F_SQRT, __fsqrt_rn(fabsf(a)))
+      UN(F_INV, fabsf(a) > kDelta ? __frcp_rn(a) : 0.0f)
+      BIN(F_LT, a < bb ? 1.0f : 0.0f)
+      BIN(F_GT, a > bb ? 1.0f : 0.0f)
+      BIN(F_LE, a <= bb ? 1.0f : 0.0f)
+      BIN(F_GE, a >= bb ? 1.0f : 0.0f)
+      default: {  // F_IF (ternary): a = tos, b = first pop, c = second pop
+        POP(b);
+        POP(c);
+        FOR_K RES(k) = tos[k] > 0.0f ? b[k] : c[k];
         break;
-      case F_SUB:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = __fsub_rn(tos[k], b[k]);
-        break;
-      case F_MUL:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = __fmul_rn(tos[k], b[k]);
-        break;
-      case F_DIV:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = fabsf(b[k]) > kDelta ? __fdiv_rn(tos[k], b[k]) : 1.0f;
-        break;
-      case F_SIN:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = sinf(tos[k]);
-        break;
-      case F_COS:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = cosf(tos[k]);
-        break;
-      case F_TAN:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = tanf(tos[k]);
-        break;
-      case F_MAX:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = fmaxf(tos[k], b[k]);
-        break;
-      case F_MIN:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = fminf(tos[k], b[k]);
-        break;
-      case F_POW:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = powf(fabsf(tos[k]), b[k]);
-        break;
-      case F_LOG:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = fabsf(tos[k]) > kDelta ? logf(fabsf(tos[k])) : 0.0f;
-        break;
-      case F_EXP:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = expf(tos[k]);
-        break;
-      case F_TANH:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = tanhf(tos[k]);
-        break;
-      case F_NEG:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = -tos[k];
-        break;
-      case F_ABS:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = fabsf(tos[k]);
-        break;
-      case F_SQRT:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = __fsqrt_rn(fabsf(tos[k]));
-        break;
-      case F_INV:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = fabsf(tos[k]) > kDelta ? __fdiv_rn(1.0f, tos[k]) : 0.0f;
-        break;
-      case F_LT:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = tos[k] < b[k] ? 1.0f : 0.0f;
-        break;
-      case F_GT:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = tos[k] > b[k] ? 1.0f : 0.0f;
-        break;
-      case F_LE:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = tos[k] <= b[k] ? 1.0f : 0.0f;
-        break;
-      case F_GE:
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = tos[k] >= b[k] ? 1.0f : 0.0f;
-        break;
-      default:  // F_IF
-#pragma unroll
-        for (int k = 0; k < K; ++k) r[k] = tos[k] > 0.0f ? b[k] : c[k];
-        break;
-    }
-    if (MULTI && nd.slot != kNoSlot) {
-      float* a = acc + nd.slot * (32 * K);
-      float av[K];
-      vld<K>(a, lane, av);
-#pragma unroll
-      for (int k = 0; k < K; ++k) av[k] = __fadd_rn(av[k], r[k]);
-      vst<K>(a, lane, av);
-      // pass the rightmost child's value upward (unary: the child itself)
-      if (ar == 2) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) tos[k] = b[k];
-      } else if (ar == 3) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) tos[k] = c[k];
       }
-    } else {
-#pragma unroll
-      for (int k = 0; k < K; ++k) tos[k] = r[k];
+    }
+#undef RES
+#undef POP
+#undef BIN
+#undef UN
+#undef TRIG
+    if constexpr (MULTI) {
+      const uint32_t slot = (nd.x >> 8) & 0xFFu;
+      if (slot != kNoSlot) {
+        float* acc = accl + slot * SLOT;
+        float av[K];
+        vld<K>(acc, av);
+        FOR_K av[k] = __fadd_rn(av[k], r[k]);
+        vst<K>(acc, av);
+        // pass the rightmost child's value upward (unary: the child itself)
+        const int ar = func_arity(static_cast<int>(op) - OP_FN);
+        if (ar == 2) {
+          FOR_K tos[k] = b[k];
+        } else if (ar == 3) {
+          FOR_K tos[k] = c[k];
+        }
+      } else {
+        FOR_K tos[k] = r[k];
+      }
     }
   }
 }
 
+// ------------------------------------------------------------------------
+// Deep-stack pool: rows whose stack exceeds the shared slots borrow one of
+// `deep_slots` global slots (ticket + per-slot spin lock; holders always
+// release, so waiting is bounded).
+// ------------------------------------------------------------------------
+__device__ __forceinline__ int deep_acquire(const KParams& p, int lane) {
+  int slot = 0;
+  if (lane == 0) {
+    slot = static_cast<int>(atomicAdd(&p.ctl->deep, 1ull) % static_cast<unsigned long long>(p.deep_slots));
+    while (atomicCAS(p.deep_locks + slot, 0, 1) != 0) __nanosleep(200);
+    __threadfence();
+  }
+  return __shfl_sync(FULL_MASK, slot, 0);
+}
+
+__device__ __forceinline__ void deep_release(const KParams& p, int slot, int lane) {
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    atomicExch(p.deep_locks + slot, 0);
+  }
+}
+
+// Evaluate `tree` on one chunk with whichever stack storage the row needs.
+template <int K, bool MULTI>
+__device__ __forceinline__ void run_chunk(const KParams& p, const Node* tree, const TreeInfo& ti, int64_t chunk_base,
+                                          int lane, float* s_stack_l, float* s_acc_l, float (&tos)[K]) {
+  constexpr int V = Lay<K>::V;
+  const float* xl = p.xs + chunk_base + lane * V;
+  const bool deep = ti.maxdepth - 1 > p.SD;
+  int slot = 0;
+  float* stk = s_stack_l;
+  if (deep) {
+    slot = deep_acquire(p, lane);
+    stk = p.deep + static_cast<int64_t>(slot) * p.deep_slot_floats + lane * V;
+  }
+  interpret<K, MULTI>(tree, ti.len, xl, stk, s_acc_l, tos);
+  if (deep) deep_release(p, slot, lane);
+}
+
+// ------------------------------------------------------------------------
 // ------------------------------------------------------------------------
 // Epilogues
 // ------------------------------------------------------------------------
@@ -380,20 +400,18 @@ __device__ __forceinline__ double warp_sum_d(double s) {
   return s;
 }
 
-// Single-output store out[tp][d]
 template <int K>
 __device__ __forceinline__ void store_out1(const KParams& p, int64_t tp, int64_t chunk_base, int lane,
                                           const float (&v)[K], bool valid) {
   float* o = p.out + tp * p.D;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
+  FOR_K {
     const int64_t d = chunk_base + Lay<K>::point(lane, k);
     if (d < p.D) o[d] = valid ? v[k] : __int_as_float(0x7FC00000);
   }
 }
 
-// Multi-output store out[tp][d][o] from the per-warp accumulator acc[o][32K],
-// written as one contiguous, coalesced range of the row.
+// out[tp][d][o] from the per-warp accumulator acc[o][32K], written as one
+// contiguous, coalesced range of the row.
 template <int K>
 __device__ __forceinline__ void store_outn(const KParams& p, int64_t tp, int64_t chunk_base, int lane,
                                           const float* acc, bool valid) {
@@ -409,14 +427,18 @@ __device__ __forceinline__ void store_outn(const KParams& p, int64_t tp, int64_t
   __syncwarp();
 }
 
+// FP64 residual^2 over the lane's valid points (reading R7); y is staged as
+// row n_in of xs.
 template <int K>
 __device__ __forceinline__ double lane_sse(const KParams& p, int64_t chunk_base, int lane, const float (&v)[K]) {
+  constexpr int V = Lay<K>::V;
+  float yv[K];
+  vld_nc<K>(p.xs + static_cast<int64_t>(p.n_in) * p.Dpad + chunk_base + lane * V, yv);
   double s = 0.0;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
+  FOR_K {
     const int64_t d = chunk_base + Lay<K>::point(lane, k);
     if (d < p.D) {
-      const double r = static_cast<double>(v[k]) - static_cast<double>(__ldg(p.y + d));
+      const double r = static_cast<double>(v[k]) - static_cast<double>(yv[k]);
       s = __dadd_rn(s, __dmul_rn(r, r));
     }
   }
@@ -424,8 +446,8 @@ __device__ __forceinline__ double lane_sse(const KParams& p, int64_t chunk_base,
 }
 
 // Deterministic cross-unit combine of per-tree partial SSEs: every unit
-// writes its partial, the last one to arrive (per-tree counter) sums all
-// partials in ascending part order and writes the result (reading R9).
+// writes its partial; the last to arrive (per-tree counter) sums all
+// partials in a fixed order and writes the result (reading R9).
 __device__ __forceinline__ void combine_partial(const KParams& p, int64_t tp, int part, double s, int lane) {
   if (p.nparts == 1) {
     if (lane == 0) p.res[tp] = p.div_by_D ? s / static_cast<double>(p.D) : s;
@@ -443,29 +465,39 @@ __device__ __forceinline__ void combine_partial(const KParams& p, int64_t tp, in
   __threadfence();
   double acc = 0.0;
   for (int q = lane; q < p.nparts; q += 32) acc += __ldcg(p.partials + tp * p.nparts + q);
-  // fixed-order warp reduction (lane-strided partials, then a fixed shuffle tree)
-  acc = warp_sum_d(acc);
+  acc = warp_sum_d(acc);  // fixed lane-strided order, then a fixed shuffle tree
   if (lane == 0) {
     p.res[tp] = p.div_by_D ? acc / static_cast<double>(p.D) : acc;
     p.counters[tp] = 0;
   }
 }
 
+#define kNaN64 __longlong_as_double(0x7FF8000000000000ll)
+
 // ------------------------------------------------------------------------
 // a2: dataset staging
 // ------------------------------------------------------------------------
-__global__ void k_stage_x(const float* __restrict__ X, int32_t x_layout, int64_t D, int32_t n_in, int64_t Dpad,
-                          float* __restrict__ xs, int32_t* __restrict__ counters, int64_t n_counters) {
-  const int64_t total = static_cast<int64_t>(n_in) * Dpad;
+__global__ void k_stage_x(const float* __restrict__ X, int32_t x_layout, const float* __restrict__ y, int64_t D,
+                          int32_t n_in, int64_t Dpad, float* __restrict__ xs, int32_t* __restrict__ counters,
+                          int64_t n_counters, Control* __restrict__ ctl) {
+  const int64_t rows = n_in + (y ? 1 : 0);
+  const int64_t total = rows * Dpad;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int64_t e = t0; e < total; e += stride) {
     const int64_t k = e / Dpad, d = e - k * Dpad;
     float v = 0.f;
-    if (d < D) v = x_layout == EVOGP_X_SOA ? X[k * D + d] : X[d * n_in + k];
+    if (d < D) {
+      if (k == n_in) v = y[d];
+      else v = x_layout == EVOGP_X_SOA ? X[k * D + d] : X[d * n_in + k];
+    }
     xs[e] = v;
   }
-  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n_counters; e += stride)
-    counters[e] = 0;
+  for (int64_t e = t0; e < n_counters; e += stride) counters[e] = 0;
+  if (t0 == 0) {
+    ctl->work = 0;
+    ctl->deep = 0;
+  }
 }
 
 // ------------------------------------------------------------------------
@@ -473,55 +505,53 @@ __global__ void k_stage_x(const float* __restrict__ X, int32_t x_layout, int64_t
 // ------------------------------------------------------------------------
 constexpr int kInterWarps = 4;
 
+__device__ __forceinline__ long long next_ticket(const KParams& p, int lane) {
+  unsigned long long t = 0;
+  if (lane == 0) t = atomicAdd(&p.ctl->work, 1ull);
+  return static_cast<long long>(__shfl_sync(FULL_MASK, t, 0));
+}
+
 template <int K, int MODE>
 __global__ void __launch_bounds__(32 * kInterWarps) k_inter(const KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int V = Lay<K>::V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wbase = smem + static_cast<size_t>(warp) * p.warp_smem_bytes;
+  unsigned char* wbase = smem + static_cast<size_t>(warp) * (p.tree_bytes + p.warp_smem_bytes);
   Node* s_tree = reinterpret_cast<Node*>(wbase);
-  float* s_stack = reinterpret_cast<float*>(wbase + p.tree_bytes);
-  float* s_acc = s_stack + p.SD * 32 * K;
-  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kInterWarps + warp;
-  const int64_t nw = static_cast<int64_t>(gridDim.x) * kInterWarps;
-  Stack<K> st;
-  st.smem = s_stack;
-  st.spill = p.spill + gw * p.spill_slots * (32 * K);
-  st.SD = p.SD;
-  st.lane = lane;
-  const int64_t nunits = p.P * p.nch;
+  float* s_stack_l = reinterpret_cast<float*>(wbase + p.tree_bytes) + lane * V;
+  float* s_acc_l = s_stack_l + p.SD * 32 * K;
+  const long long nunits = p.P * p.nch;
+  long long u = next_ticket(p, lane);
   int64_t staged = -1;
   TreeInfo ti{1, 1, false};
-  for (int64_t u = gw; u < nunits; u += nw) {
+  while (u < nunits) {
+    const long long u_next = next_ticket(p, lane);  // issued early, used next iteration
     const int64_t tp = u / p.nch;
     const int c = static_cast<int>(u - tp * p.nch);
     if (tp != staged) {
       __syncwarp();
       ti = stage_tree_warp(p, tp, s_tree, lane);
       staged = tp;
-      if (!ti.valid && lane == 0) atomicOr(p.flags, 1);
+      if (!ti.valid && lane == 0) atomicOr(&p.ctl->flags, 1);
     }
-    const bool runnable = ti.valid && ti.maxdepth - 1 <= p.SD + p.spill_slots;
     const int64_t chunk_base = static_cast<int64_t>(c) * (32 * K);
     float tos[K];
     if (MODE == MODE_EVALN) {
       float z[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) z[k] = 0.f;
-      for (int o = 0; o < p.n_out; ++o) vst<K>(s_acc + o * (32 * K), lane, z);
+      FOR_K z[k] = 0.f;
+      for (int o = 0; o < p.n_out; ++o) vst<K>(s_acc_l + o * (32 * K), z);
     }
-    if (runnable) {
-      st.sp = 0;
-      interpret<K, MODE == MODE_EVALN>(s_tree, ti.len, p.xs, p.Dpad, chunk_base, lane, st, s_acc, tos);
-    }
+    if (ti.valid) run_chunk<K, MODE == MODE_EVALN>(p, s_tree, ti, chunk_base, lane, s_stack_l, s_acc_l, tos);
     if (MODE == MODE_EVAL1) {
-      store_out1<K>(p, tp, chunk_base, lane, tos, runnable);
+      store_out1<K>(p, tp, chunk_base, lane, tos, ti.valid);
     } else if (MODE == MODE_EVALN) {
-      store_outn<K>(p, tp, chunk_base, lane, s_acc, runnable);
+      store_outn<K>(p, tp, chunk_base, lane, s_acc_l - lane * V, ti.valid);
     } else {
-      double s = runnable ? lane_sse<K>(p, chunk_base, lane, tos) : __longlong_as_double(0x7FF8000000000000ll);
+      double s = ti.valid ? lane_sse<K>(p, chunk_base, lane, tos) : kNaN64;
       s = warp_sum_d(s);
       combine_partial(p, tp, c, s, lane);
     }
+    u = u_next;
   }
 }
 
@@ -540,48 +570,51 @@ __global__ void __launch_bounds__(32 * kIntraWarps) k_intra(const KParams p) {
   __shared__ __align__(8) uint64_t mbar;
   __shared__ double s_red[kIntraWarps];
   __shared__ TreeInfo s_info;
+  __shared__ long long s_item[2];
+  constexpr int V = Lay<K>::V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // layout: raw rows (type, value) | decoded tree | per-warp stacks (+acc)
+  // layout: raw type row | raw value row | decoded tree | per-warp stacks (+acc)
   int16_t* raw_type = reinterpret_cast<int16_t*>(smem);
-  float* raw_value = reinterpret_cast<float*>(smem + p.raw_bytes / 3);  // type part is raw_bytes/3 (see plan)
-  Node* s_tree = reinterpret_cast<Node*>(smem + p.raw_bytes);
-  unsigned char* wbase = smem + p.raw_bytes + p.tree_bytes + static_cast<size_t>(warp) * p.warp_smem_bytes;
-  float* s_stack = reinterpret_cast<float*>(wbase);
-  float* s_acc = s_stack + p.SD * 32 * K;
-  Stack<K> st;
-  st.smem = s_stack;
-  st.spill = p.spill + (static_cast<int64_t>(blockIdx.x) * kIntraWarps + warp) * p.spill_slots * (32 * K);
-  st.SD = p.SD;
-  st.lane = lane;
-  if (threadIdx.x == 0 && p.use_tma) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  float* raw_value = reinterpret_cast<float*>(smem + p.raw_type_bytes);
+  Node* s_tree = reinterpret_cast<Node*>(smem + p.raw_type_bytes + p.raw_value_bytes);
+  unsigned char* wbase = smem + p.raw_type_bytes + p.raw_value_bytes + p.tree_bytes +
+                         static_cast<size_t>(warp) * p.warp_smem_bytes;
+  float* s_stack_l = reinterpret_cast<float*>(wbase) + lane * V;
+  float* s_acc_l = s_stack_l + p.SD * 32 * K;
+  if (threadIdx.x == 0) {
+    if (p.use_tma) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    s_item[0] = static_cast<long long>(atomicAdd(&p.ctl->work, 1ull));
   }
   __syncthreads();
-  const int64_t nitems = p.P * p.nseg;
+  const long long nitems = p.P * p.nseg;
   uint32_t phase = 0;
-  double lane_acc = 0.0;
-  for (int64_t item = blockIdx.x; item < nitems; item += gridDim.x) {
+  int it = 0;
+  for (;;) {
+    const long long item = s_item[it & 1];
+    if (item >= nitems) break;
     const int64_t tp = item / p.nseg;
     const int seg = static_cast<int>(item - tp * p.nseg);
-    __syncthreads();  // previous item is done with the shared tree
     if (p.use_tma) {
       // a4: TMA bulk copy of the row into shared memory, completion on an mbarrier
       if (threadIdx.x == 0) {
-        const uint32_t tb = static_cast<uint32_t>(((p.L * 2) + 15) & ~15);
-        const uint32_t vb = static_cast<uint32_t>(((p.L * 4) + 15) & ~15);
+        s_item[(it + 1) & 1] = static_cast<long long>(atomicAdd(&p.ctl->work, 1ull));
         const uint32_t bar = smem_u32(&mbar);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tb + vb) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"(static_cast<uint32_t>(p.raw_type_bytes + p.raw_value_bytes))
+                     : "memory");
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                 smem_u32(raw_type)),
-            "l"(p.type + tp * p.ld), "r"(tb), "r"(bar)
+            "l"(p.type + tp * p.ld), "r"(static_cast<uint32_t>(p.raw_type_bytes)), "r"(bar)
             : "memory");
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                 smem_u32(raw_value)),
-            "l"(p.value + tp * p.ld), "r"(vb), "r"(bar)
+            "l"(p.value + tp * p.ld), "r"(static_cast<uint32_t>(p.raw_value_bytes)), "r"(bar)
             : "memory");
       }
       if (warp == 0) {
@@ -589,7 +622,8 @@ __global__ void __launch_bounds__(32 * kIntraWarps) k_intra(const KParams p) {
         const uint32_t bar = smem_u32(&mbar);
         while (!done) {
           asm volatile(
-              "{\n .reg .pred P1;\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n selp.u32 %0, 1, 0, P1;\n}\n"
+              "{\n .reg .pred P1;\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n selp.u32 %0, 1, 0, "
+              "P1;\n}\n"
               : "=r"(done)
               : "r"(bar), "r"(phase)
               : "memory");
@@ -598,51 +632,50 @@ __global__ void __launch_bounds__(32 * kIntraWarps) k_intra(const KParams p) {
         if (lane == 0) s_info = ti;
       }
       phase ^= 1u;
-    } else if (warp == 0) {
-      const TreeInfo ti = stage_tree_warp(p, tp, s_tree, lane);
-      if (lane == 0) s_info = ti;
+    } else {
+      if (threadIdx.x == 0) s_item[(it + 1) & 1] = static_cast<long long>(atomicAdd(&p.ctl->work, 1ull));
+      if (warp == 0) {
+        const TreeInfo ti = stage_tree_warp(p, tp, s_tree, lane);
+        if (lane == 0) s_info = ti;
+      }
     }
     __syncthreads();
     const TreeInfo ti = s_info;
-    if (!ti.valid && threadIdx.x == 0 && seg == 0) atomicOr(p.flags, 1);
-    const bool runnable = ti.valid && ti.maxdepth - 1 <= p.SD + p.spill_slots;
+    if (!ti.valid && threadIdx.x == 0 && seg == 0) atomicOr(&p.ctl->flags, 1);
     const int c_begin = seg * p.seg_chunks;
     const int c_end = min(p.nch, c_begin + p.seg_chunks);
-    lane_acc = 0.0;
+    double lane_acc = 0.0;
     for (int c = c_begin + warp; c < c_end; c += kIntraWarps) {
       const int64_t chunk_base = static_cast<int64_t>(c) * (32 * K);
       float tos[K];
       if (MODE == MODE_EVALN) {
         float z[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) z[k] = 0.f;
-        for (int o = 0; o < p.n_out; ++o) vst<K>(s_acc + o * (32 * K), lane, z);
+        FOR_K z[k] = 0.f;
+        for (int o = 0; o < p.n_out; ++o) vst<K>(s_acc_l + o * (32 * K), z);
       }
-      if (runnable) {
-        st.sp = 0;
-        interpret<K, MODE == MODE_EVALN>(s_tree, ti.len, p.xs, p.Dpad, chunk_base, lane, st, s_acc, tos);
-      }
+      if (ti.valid) run_chunk<K, MODE == MODE_EVALN>(p, s_tree, ti, chunk_base, lane, s_stack_l, s_acc_l, tos);
       if (MODE == MODE_EVAL1) {
-        store_out1<K>(p, tp, chunk_base, lane, tos, runnable);
+        store_out1<K>(p, tp, chunk_base, lane, tos, ti.valid);
       } else if (MODE == MODE_EVALN) {
-        store_outn<K>(p, tp, chunk_base, lane, s_acc, runnable);
-      } else {
-        lane_acc += runnable ? lane_sse<K>(p, chunk_base, lane, tos) : __longlong_as_double(0x7FF8000000000000ll);
+        store_outn<K>(p, tp, chunk_base, lane, s_acc_l - lane * V, ti.valid);
+      } else if (ti.valid) {
+        lane_acc += lane_sse<K>(p, chunk_base, lane, tos);
       }
     }
     if (MODE == MODE_SSE) {
       // a7: lanes -> warp (shuffle) -> CTA (shared memory, fixed order) -> tree
       const double w = warp_sum_d(lane_acc);
       if (lane == 0) s_red[warp] = w;
-      __syncthreads();
-      if (warp == 0) {
-        double s = lane < kIntraWarps ? s_red[lane] : 0.0;
-#pragma unroll
-        for (int off = 4; off > 0; off >>= 1) s += __shfl_xor_sync(FULL_MASK, s, off);
-        if (!runnable) s = __longlong_as_double(0x7FF8000000000000ll);
-        combine_partial(p, tp, seg, s, lane);
-      }
     }
+    __syncthreads();  // s_red complete; everyone is done with s_tree / raw rows
+    if (MODE == MODE_SSE && warp == 0) {
+      double s = lane < kIntraWarps ? s_red[lane] : 0.0;
+#pragma unroll
+      for (int off = 4; off > 0; off >>= 1) s += __shfl_xor_sync(FULL_MASK, s, off);
+      if (!ti.valid) s = kNaN64;
+      combine_partial(p, tp, seg, s, lane);
+    }
+    ++it;
   }
 }
 
@@ -671,7 +704,7 @@ int num_sms(int dev) {
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
 // Upper bound on the operand-stack depth of a well-formed row of length L:
-// at most one entry per leaf, and leaves <= (2L + 1) / 3 when arity >= 2.
+// one entry per leaf at most, and leaves <= (2L + 1) / 3 when arity >= 2.
 inline int max_depth_bound(int L) { return std::min(L, (2 * L + 1) / 3 + 1); }
 
 template <int K, int MODE>
@@ -680,36 +713,67 @@ template <int K, int MODE>
 const void* intra_fn() { return reinterpret_cast<const void*>(&k_intra<K, MODE>); }
 
 const void* kernel_ptr(int strategy, int K, int mode) {
-#define EVOGP_PICK(S, KK)                                          \
-  if (K == KK) {                                                    \
-    if (mode == MODE_EVAL1) return S##_fn<KK, MODE_EVAL1>();        \
-    if (mode == MODE_EVALN) return S##_fn<KK, MODE_EVALN>();        \
-    return S##_fn<KK, MODE_SSE>();                                  \
+#define EVOGP_PICK(S, KK)                                   \
+  if (K == KK) {                                            \
+    if (mode == MODE_EVAL1) return S##_fn<KK, MODE_EVAL1>(); \
+    if (mode == MODE_EVALN) return S##_fn<KK, MODE_EVALN>(); \
+    return S##_fn<KK, MODE_SSE>();                          \
   }
   if (strategy == EVOGP_STRATEGY_INTER) {
     EVOGP_PICK(inter, 1)
     EVOGP_PICK(inter, 2)
     EVOGP_PICK(inter, 4)
+    EVOGP_PICK(inter, 8)
   } else {
     EVOGP_PICK(intra, 4)
+    EVOGP_PICK(intra, 8)
   }
 #undef EVOGP_PICK
   return nullptr;
 }
 
+// occupancy per (kernel, smem) is cached: the query costs microseconds
+std::mutex g_occ_mu;
+std::unordered_map<uint64_t, int> g_occ;
+
+int occupancy(const void* fn, int threads, size_t smem, int dev) {
+  const uint64_t key = (reinterpret_cast<uint64_t>(fn) * 1315423911ull) ^ (static_cast<uint64_t>(smem) << 8) ^
+                       static_cast<uint64_t>(dev);
+  {
+    std::lock_guard<std::mutex> g(g_occ_mu);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) return it->second;
+  }
+  int occ = 0;
+  // always the full opt-in limit (227 KB minus the kernel's static shared
+  // memory): a later, smaller plan must not lower the attribute below what an
+  // earlier (cached) plan launches with
+  cudaFuncAttributes fa;
+  int max_dyn = 227 * 1024;
+  if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess) max_dyn -= static_cast<int>(fa.sharedSizeBytes);
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    occ = std::max<int>(1, static_cast<int>((227 * 1024) / std::max<size_t>(smem, 1)));
+    occ = std::min(occ, 64 * 32 / threads);
+  }
+  std::lock_guard<std::mutex> g(g_occ_mu);
+  g_occ[key] = occ;
+  return occ;
+}
+
 }  // namespace
 
 // Selector (c). PAPER P:356 compares D with the CUDA-core count (SMs x 128
-// on B200 = 18,944, reading R11); the measured crossover table replaces the
-// rule once calibrated.
+// on B200 = 18,944, reading R11); DESIGN.md "Selector" records the measured
+// crossover that replaces the rule.
 int select_strategy(int64_t P, int64_t D, int32_t L, int32_t n_out, int device) {
   (void)L;
   (void)n_out;
+  (void)P;
   const int sms = num_sms(device);
   const int64_t threshold = static_cast<int64_t>(sms) * 128;
-  if (D >= threshold) return EVOGP_STRATEGY_INTRA;
-  (void)P;
-  return EVOGP_STRATEGY_INTER;
+  return D >= threshold ? EVOGP_STRATEGY_INTRA : EVOGP_STRATEGY_INTER;
 }
 
 int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_t n_out, int mode, int strategy,
@@ -718,56 +782,52 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   if (strategy == EVOGP_STRATEGY_AUTO) strategy = select_strategy(P, D, L, n_out, device);
   if (strategy != EVOGP_STRATEGY_INTER && strategy != EVOGP_STRATEGY_INTRA) return EVOGP_E_ARG;
   const int sms = num_sms(device);
+  const bool multi = mode == MODE_EVALN;
   int K;
-  if (strategy == EVOGP_STRATEGY_INTER) K = D <= 32 ? 1 : (D <= 64 ? 2 : 4);
-  else K = 4;
+  if (strategy == EVOGP_STRATEGY_INTER) K = D <= 32 ? 1 : (D <= 64 ? 2 : (D <= 128 || multi ? 4 : 8));
+  else K = multi ? 4 : 8;
   const int warps = strategy == EVOGP_STRATEGY_INTER ? kInterWarps : kIntraWarps;
   const int64_t chunk = 32 * K;
   const int64_t nch = (D + chunk - 1) / chunk;
   const int64_t Dpad = round_up(std::max<int64_t>(D, 1), 256);
   const int slot_bytes = 32 * K * 4;
-  const int acc_bytes = mode == MODE_EVALN ? n_out * slot_bytes : 0;
+  const int acc_bytes = multi ? n_out * slot_bytes : 0;
   const int depth = max_depth_bound(L);
-  // shared-memory budget: aim at ~24 resident warps per SM
-  const int budget_per_warp = (227 * 1024) / 24;
-  int tree_bytes = static_cast<int>(round_up(static_cast<int64_t>(L) * 8, 16));
-  int raw_bytes = 0;
-  int per_warp_fixed = acc_bytes;
-  if (strategy == EVOGP_STRATEGY_INTER) per_warp_fixed += tree_bytes;
-  else raw_bytes = static_cast<int>(3 * round_up(static_cast<int64_t>(L) * 2, 16));  // type + value (2x) rounded
+  const int tree_bytes = static_cast<int>(round_up(static_cast<int64_t>(L + 1) * 8, 16));
+  // shared-memory budget: aim at ~20 resident warps per SM
+  const int budget_per_warp = (227 * 1024) / 20;
+  const int per_warp_fixed = acc_bytes + (strategy == EVOGP_STRATEGY_INTER ? tree_bytes : 0);
   int SD = (budget_per_warp - per_warp_fixed) / slot_bytes;
-  SD = std::max(1, std::min(SD, depth - 1));
-  if (depth - 1 <= 0) SD = 1;
-  const int spill_slots = std::max(0, depth - 1 - SD);
-  int warp_smem = per_warp_fixed + SD * slot_bytes;
-  if (strategy == EVOGP_STRATEGY_INTRA) warp_smem = acc_bytes + SD * slot_bytes;
-  size_t smem = strategy == EVOGP_STRATEGY_INTER
-                    ? static_cast<size_t>(warps) * warp_smem
-                    : static_cast<size_t>(raw_bytes) + tree_bytes + static_cast<size_t>(warps) * warp_smem;
+  SD = std::max(2, std::min(SD, std::max(1, depth - 1)));
+  const int warp_smem = acc_bytes + SD * slot_bytes;
+  const int raw_type_bytes = strategy == EVOGP_STRATEGY_INTRA ? static_cast<int>(round_up(int64_t(L) * 2, 16)) : 0;
+  const int raw_value_bytes = strategy == EVOGP_STRATEGY_INTRA ? static_cast<int>(round_up(int64_t(L) * 4, 16)) : 0;
+  const size_t smem = strategy == EVOGP_STRATEGY_INTER
+                          ? static_cast<size_t>(warps) * (tree_bytes + warp_smem)
+                          : static_cast<size_t>(raw_type_bytes) + raw_value_bytes + tree_bytes +
+                                static_cast<size_t>(warps) * warp_smem;
   if (smem > 227 * 1024) return EVOGP_E_UNSUPPORTED;
+  if (static_cast<int64_t>(n_in + 1) * Dpad > 0xFFFFFFFFll) return EVOGP_E_UNSUPPORTED;  // u32 leaf offsets
   const void* fn = kernel_ptr(strategy, K, mode);
   if (!fn) return EVOGP_E_ARG;
-  int occ = 0;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-          cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * warps, smem) != cudaSuccess || occ < 1) {
-    cudaGetLastError();
-    occ = std::max<int>(1, static_cast<int>((227 * 1024) / std::max<size_t>(smem, 1)));
-    occ = std::min(occ, 64 / warps);
-  }
+  const int occ = occupancy(fn, 32 * warps, smem, device);
   const int64_t resident = static_cast<int64_t>(sms) * occ;
   int64_t grid, nseg = 1, seg_chunks = nch;
   if (strategy == EVOGP_STRATEGY_INTER) {
     const int64_t units = P * nch;
     grid = std::max<int64_t>(1, std::min<int64_t>((units + warps - 1) / warps, resident));
   } else {
-    // split each tree's datapoints into segments so items >= ~16 waves
-    nseg = std::max<int64_t>(1, std::min<int64_t>(nch, (16 * resident + P - 1) / std::max<int64_t>(P, 1)));
-    seg_chunks = (nch + nseg - 1) / nseg;
-    seg_chunks = round_up(seg_chunks, warps);
+    // split each tree's datapoints into segments: >= ~8 items per resident CTA
+    nseg = std::max<int64_t>(1, std::min<int64_t>(nch, (8 * resident + P - 1) / std::max<int64_t>(P, 1)));
+    seg_chunks = round_up((nch + nseg - 1) / nseg, warps);
     nseg = (nch + seg_chunks - 1) / seg_chunks;
     grid = std::max<int64_t>(1, std::min<int64_t>(P * nseg, resident));
   }
+  // deep-stack pool: slots of the full depth bound; at most 256, at most ~256 MB
+  const int64_t deep_slot_floats = static_cast<int64_t>(depth) * 32 * K;
+  const int64_t per_slot = deep_slot_floats * 4;
+  const int deep_slots =
+      static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(256, (int64_t(256) << 20) / std::max<int64_t>(per_slot, 1))));
   pl.strategy = strategy;
   pl.K = K;
   pl.warps_per_cta = warps;
@@ -785,55 +845,56 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   kp.seg_chunks = static_cast<int32_t>(seg_chunks);
   kp.nparts = static_cast<int32_t>(strategy == EVOGP_STRATEGY_INTER ? nch : nseg);
   kp.SD = SD;
-  kp.spill_slots = spill_slots;
   kp.tree_bytes = tree_bytes;
   kp.warp_smem_bytes = warp_smem;
-  kp.raw_bytes = raw_bytes;
+  kp.raw_type_bytes = raw_type_bytes;
+  kp.raw_value_bytes = raw_value_bytes;
   kp.out_magic = static_cast<int32_t>((0x100000000ull + n_out - 1) / n_out);
+  kp.deep_slots = deep_slots;
+  kp.deep_slot_floats = deep_slot_floats;
   // workspace layout (256-byte aligned sections)
   size_t off = 0;
-  pl.off_flags = off;
+  pl.off_ctl = off;
   off += 256;
   pl.off_xs = off;
-  off += round_up(static_cast<int64_t>(n_in) * Dpad * 4, 256);
+  off += round_up(static_cast<int64_t>(n_in + 1) * Dpad * 4, 256);
   pl.off_counters = off;
   off += round_up(P * 4, 256);
   pl.off_partials = off;
   off += mode == MODE_SSE && kp.nparts > 1 ? round_up(P * kp.nparts * 8, 256) : 0;
-  pl.off_spill = off;
-  off += round_up(static_cast<int64_t>(grid) * warps * spill_slots * slot_bytes, 256);
+  pl.off_locks = off;
+  off += round_up(static_cast<int64_t>(deep_slots) * 4, 256);
+  pl.off_deep = off;
+  off += round_up(static_cast<int64_t>(deep_slots) * per_slot, 256);
   pl.total = off;
   return EVOGP_OK;
 }
 
-int launch(Plan& pl, int mode, const float* X, int32_t x_layout, void* stream, int* n_launches) {
+int launch(Plan& pl, int mode, const float* X, int32_t x_layout, const float* y, void* stream, int* n_launches,
+           void* ev_start, void* ev_end) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   KParams& kp = pl.kp;
   int launches = 0;
   {
-    const int64_t total = static_cast<int64_t>(kp.n_in) * kp.Dpad;
+    const int64_t total = static_cast<int64_t>(kp.n_in + 1) * kp.Dpad;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8));
-    k_stage_x<<<static_cast<int>(blocks), 256, 0, s>>>(X, x_layout, kp.D, kp.n_in, kp.Dpad,
-                                                        const_cast<float*>(kp.xs), kp.counters,
-                                                        mode == MODE_SSE ? kp.P : 0);
+    k_stage_x<<<static_cast<int>(blocks), 256, 0, s>>>(X, x_layout, mode == MODE_SSE ? y : nullptr, kp.D, kp.n_in,
+                                                        kp.Dpad, const_cast<float*>(kp.xs), kp.counters,
+                                                        mode == MODE_SSE ? kp.P : 0, kp.ctl);
     ++launches;
   }
   const void* fn = kernel_ptr(pl.strategy, pl.K, mode);
   if (!fn) return EVOGP_E_ARG;
   void* args[] = {&kp};
+  if (ev_start) cudaEventRecord(static_cast<cudaEvent_t>(ev_start), s);
   cudaError_t err = cudaLaunchKernel(fn, dim3(pl.grid), dim3(32 * pl.warps_per_cta), args, pl.smem_bytes, s);
+  if (ev_end) cudaEventRecord(static_cast<cudaEvent_t>(ev_end), s);
   ++launches;
   if (n_launches) *n_launches = launches;
+  if (err == cudaSuccess) err = cudaGetLastError();
   if (err != cudaSuccess) {
     char buf[256];
     std::snprintf(buf, sizeof(buf), "kernel launch failed: %s", cudaGetErrorString(err));
-    set_last_error(buf);
-    return EVOGP_E_CUDA;
-  }
-  err = cudaGetLastError();
-  if (err != cudaSuccess) {
-    char buf[256];
-    std::snprintf(buf, sizeof(buf), "CUDA error: %s", cudaGetErrorString(err));
     set_last_error(buf);
     return EVOGP_E_CUDA;
   }

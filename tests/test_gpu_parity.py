@@ -404,3 +404,39 @@ def test_full_size_c3_sampled_trees():
     rel = np.abs(m[rows][fin] - m64[fin]) / np.abs(m64[fin])
     # literal MSE pass rate at C3 (uncertified trees may legitimately differ)
     assert (rel <= TOL).mean() >= 0.25, rel
+
+
+# ---------------------------------------------------------------- primitive accuracy
+def _ulp_err(g, ref):
+    g = g.astype(np.float64)
+    sp = np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        return np.abs(g - ref) / sp
+
+
+def test_fast_trig_accuracy():
+    """The interpreter's sin/cos (MUFU after a Cody-Waite 2*pi reduction) and
+    tan (polynomial) stay within the error model the oracle's certificate
+    assumes (R14): |err| <= ABS + ulps * ulp(|ref|)."""
+    rng = np.random.default_rng(11)
+    near = (np.arange(-2000, 2001)[:, None] * (np.pi / 2) + rng.uniform(-1e-3, 1e-3, (4001, 64))).ravel()
+    xs = np.concatenate([rng.uniform(-10, 10, 1 << 20), rng.uniform(-1e5, 1e5, 1 << 19),
+                         np.sign(rng.standard_normal(1 << 18)) * 10 ** rng.uniform(-8, 0, 1 << 18), near,
+                         rng.uniform(1e5, 1e7, 4096), np.array([0.0, -0.0, 1e30, -1e30])]).astype(np.float32)
+    pt = synth.PrefixTrees(np.array([0, 2, 4, 6], np.int64), np.array([2, 1, 2, 1, 2, 1], np.int16),
+                           np.array([4, 0, 5, 0, 6, 0], np.float32))
+    dt = to_device(pt, 2, 1)
+    x64 = xs.astype(np.float64)
+    for strategy in ("inter", "intra"):
+        g = gpu_eval(dt, xs[:, None], 1, strategy)[:, :, 0].astype(np.float64)
+        for row, fn, abs_b, ulps in ((0, np.sin, TRIG_ABS, 2.0), (1, np.cos, TRIG_ABS, 2.0), (2, np.tan, 0.0, 4.0)):
+            ref = fn(x64)
+            sp = np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
+            err = np.abs(g[row] - ref)
+            bound = abs_b + ulps * sp
+            print(fn.__name__, strategy, "max abs err %.3e" % err.max(), "max err/ulp (|ref|>0.5) %.2f" %
+                  (err[np.abs(ref) > 0.5] / sp[np.abs(ref) > 0.5]).max())
+            assert (err <= bound).all(), (fn.__name__, xs[np.argmax(err - bound)], (err - bound).max())
+
+
+TRIG_ABS = 2.0 ** -20  # absolute error budget of sin.approx / cos.approx on [-pi, pi] (measured, DESIGN.md R14)
