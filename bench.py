@@ -316,6 +316,9 @@ def main():
     clocks = sampler.stop()
     step_ms = sum(a.elapsed_time(b) for a, b in ev)
     kern_ms = sum(a.elapsed_time(b) for a, b in kev)
+    # diagnostic: chunks of the last step that were re-run on the cold interpreter copy
+    off = ws.ptr - ws.buf.data_ptr()
+    cold_chunks = int(ws.buf[off + 4: off + 8].view(torch.int32).item())
     tt = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device=dev)
     work = torch.tensor([float(nodes) * D_local], dtype=torch.float64, device=dev)
     if world > 1:
@@ -380,6 +383,7 @@ def main():
                        "max_len": cfg.max_len, "n_inputs": cfg.n_in, "n_outputs": cfg.n_out,
                        "mean_len": nodes / max(1, P_local), "sfu_node_fraction": sfu_frac,
                        "strategy": chosen, "parallelism": f"{axis}-shard x{world}",
+                       "cold_rerun_chunks_last_step": cold_chunks,
                        "l2": "flushed (256 MiB write) before every timed step",
                        "step": ("evogp_eval" if cfg.n_out > 1 else "evogp_sr_fitness") +
                                (" + NCCL combine" if world > 1 else "")},

@@ -47,7 +47,7 @@ enum Mode : int { MODE_EVAL1 = 0, MODE_EVALN = 1, MODE_SSE = 2 };
 // Layout of the small control block at the start of the workspace.
 struct Control {
   int32_t flags;            // device flags (bit 0: malformed row evaluated as NaN)
-  int32_t pad;
+  uint32_t cold_chunks;     // chunks re-run on the cold interpreter copy (diagnostic, per call)
   unsigned long long work;  // dynamic work-queue ticket counter (zeroed by k_stage_x)
   unsigned long long deep;  // deep-stack pool ticket counter
 };

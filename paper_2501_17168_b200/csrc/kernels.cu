@@ -203,32 +203,26 @@ __device__ __forceinline__ void vld_nc(const float* p, float (&v)[K]) {
 }
 
 // ------------------------------------------------------------------------
-// Heavy library functions stay out of line (one copy, called per element):
-// inlining them K times per case would blow the loop's instruction footprint
-// far past the instruction caches.
-// ------------------------------------------------------------------------
-__device__ __noinline__ float call_pow(float a, float b) { return powf(fabsf(a), b); }
-__device__ __noinline__ float call_log(float a) { return fabsf(a) > kDelta ? logf(fabsf(a)) : 0.0f; }
-__device__ __noinline__ float call_tanh(float a) { return tanhf(a); }
-
-// ------------------------------------------------------------------------
 // The interpreter: evaluate one staged tree on the lane's K datapoints of
 // one chunk (nodes from len-1 down to 0; first pop = leftmost child).
-// The top of the stack lives in registers (tos); the rest behind `stk`, a
-// lane-adjusted generic pointer into shared memory or, for rows deeper than
-// the shared slots, into a global deep-stack slot (chosen per tree, so there
-// is no per-push check and a single copy of the loop).
+// The top of the stack lives in registers (tos), the rest behind `stk`, a
+// lane-adjusted pointer (shared memory in the hot copy; shared or a global
+// deep-stack slot in the cold copy).
 // MULTI: a Modi node adds its value to acc[slot] and passes its rightmost
 // child's value to the parent (reading R4).
 // FP32 with explicit round-to-nearest intrinsics (no contraction across
-// nodes); IEEE-exact + - * / sqrt; fastmath.cuh sin/cos/tan; CUDA libm for
-// the others (reading R5).
+// nodes); IEEE-exact + - * / sqrt; fastmath.cuh for the elementary
+// functions (reading R5, R14).
+// COLD = false: the hot copy — no call sites; returns true if some value left
+//   a fast path's valid range (the caller then re-runs the chunk cold).
+// COLD = true: same fast paths where valid, library functions elsewhere.
 // ------------------------------------------------------------------------
-template <int K, bool MULTI>
-__device__ __forceinline__ void interpret(const Node* __restrict__ tree, int len, const float* __restrict__ xl,
+template <int K, bool MULTI, bool COLD>
+__device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len, const float* __restrict__ xl,
                                           float* stk, float* accl, float (&tos)[K]) {
   constexpr int SLOT = 32 * K;
   float* top = stk;
+  bool bail = false;
   {
     const Node nd = tree[len];  // node len-1: a well-formed row ends with a leaf
     if ((nd.w0 & 0xFFu) == OP_CONST) {
@@ -254,72 +248,186 @@ __device__ __forceinline__ void interpret(const Node* __restrict__ tree, int len
       }
       continue;
     }
-    float b[K], c[K], r[K];
-    // RES: where a function writes its value — straight into tos unless a
-    // Modi epilogue still needs the operands
+    // Operands live only inside their case. Single-output: results go
+    // straight into tos. MULTI: results go to r; a Modi node adds r to
+    // acc[slot] and passes its rightmost child's value upward (unary: the
+    // child itself), otherwise r becomes the new top.
+#define MODI_FIN(RIGHT)                        \
+  if constexpr (MULTI) {                       \
+    const uint32_t slot = (nd.x >> 8) & 0xFFu; \
+    if (slot != kNoSlot) {                     \
+      float* acc = accl + slot * SLOT;         \
+      float av[K];                             \
+      vld<K>(acc, av);                         \
+      FOR_K av[k] = __fadd_rn(av[k], r[k]);    \
+      vst<K>(acc, av);                         \
+      FOR_K tos[k] = RIGHT[k];                 \
+    } else {                                   \
+      FOR_K tos[k] = r[k];                     \
+    }                                          \
+  }
 #define RES(k) (MULTI ? r[k] : tos[k])
 #define POP(v)   \
   top -= SLOT;   \
   vld<K>(top, v)
 #define BIN(F, EXPR)                     \
   case OP_FN + F: {                      \
+    float b[K], r[K];                    \
     POP(b);                              \
     FOR_K {                              \
       const float a = tos[k], bb = b[k]; \
       RES(k) = (EXPR);                   \
     }                                    \
+    MODI_FIN(b)                          \
+    (void)r;                             \
     break;                               \
   }
 #define UN(F, EXPR)           \
   case OP_FN + F: {           \
+    float r[K];               \
     FOR_K {                   \
       const float a = tos[k]; \
       RES(k) = (EXPR);        \
     }                         \
+    MODI_FIN(tos)             \
+    (void)r;                  \
     break;                    \
   }
-// trig: one range check per node (max |x| over the lane's K points); the
-// per-element slow path runs only when some point is out of the fast range
-#define TRIG(F, FAST, SLOW)                                               \
-  case OP_FN + F: {                                                       \
-    float m = 0.0f;                                                       \
-    FOR_K m = fmaxf(m, fabsf(tos[k]));                                    \
-    if (m <= kTrigReduceMax) {                                            \
-      FOR_K RES(k) = FAST(tos[k]);                                        \
-    } else {                                                              \
-      FOR_K {                                                             \
-        const float a = tos[k];                                           \
-        RES(k) = fabsf(a) <= kTrigReduceMax ? FAST(a) : SLOW(a);          \
-      }                                                                   \
-    }                                                                     \
-    break;                                                                \
+// range-checked unary: one check per node (max |x| over the K points)
+#define UN_RANGED(F, OK_MAX, FAST, SLOW_EXPR)                    \
+  case OP_FN + F: {                                              \
+    float r[K];                                                  \
+    float m = 0.0f;                                              \
+    FOR_K m = fmaxf(m, fabsf(tos[k]));                           \
+    if constexpr (COLD) {                                        \
+      FOR_K {                                                    \
+        const float a = tos[k];                                  \
+        RES(k) = fabsf(a) <= OK_MAX ? FAST(a) : (SLOW_EXPR);     \
+      }                                                          \
+    } else {                                                     \
+      bail |= !(m <= OK_MAX);                                    \
+      FOR_K RES(k) = FAST(tos[k]);                               \
+    }                                                            \
+    MODI_FIN(tos)                                                \
+    (void)r;                                                     \
+    (void)m;                                                     \
+    break;                                                       \
   }
     switch (op) {
       BIN(F_ADD, __fadd_rn(a, bb))
       BIN(F_SUB, __fsub_rn(a, bb))
       BIN(F_MUL, __fmul_rn(a, bb))
-      BIN(F_DIV, fabsf(bb) > kDelta ? __fdiv_rn(a, bb) : 1.0f)
-      TRIG(F_SIN, fm_sin_fast, slow_sinf)
-      TRIG(F_COS, fm_cos_fast, slow_cosf)
-      TRIG(F_TAN, fm_tan_fast, slow_tanf)
+      case OP_FN + F_DIV: {  // |b| > delta ? a / b : 1
+        float b[K], r[K];
+        POP(b);
+        // fast path: |a|, |b| <= 2^60 and a == 0 or |a| >= 2^-60; "|a| - 1ulp"
+        // as an unsigned integer makes 0 wrap to the top, so one unsigned min
+        // catches only the tiny non-zero a
+        float mx = 0.0f;
+        uint32_t mn = 0xFFFFFFFFu;
+        FOR_K {
+          mx = fmaxf(mx, fmaxf(fabsf(tos[k]), fabsf(b[k])));
+          mn = min(mn, (__float_as_uint(tos[k]) & 0x7FFFFFFFu) - 1u);
+        }
+        if constexpr (COLD) {
+          FOR_K {
+            const float a = tos[k], bb = b[k];
+            const bool fast = fabsf(a) <= kDivRange && fabsf(bb) <= kDivRange &&
+                              (a == 0.0f || fabsf(a) >= kDivRangeMin);
+            RES(k) = fabsf(bb) > kDelta ? (fast ? div_fast(a, bb) : slow_div(a, bb)) : 1.0f;
+          }
+        } else {
+          bail |= !(mx <= kDivRange) || mn < __float_as_uint(kDivRangeMin) - 1u;
+          FOR_K RES(k) = fabsf(b[k]) > kDelta ? div_fast(tos[k], b[k]) : 1.0f;
+        }
+        MODI_FIN(b)
+        (void)r;
+        break;
+      }
+      UN_RANGED(F_SIN, kTrigReduceMax, fm_sin_fast, slow_sinf(a))
+      UN_RANGED(F_COS, kTrigReduceMax, fm_cos_fast, slow_cosf(a))
+      UN_RANGED(F_TAN, kTrigReduceMax, fm_tan_fast, slow_tanf(a))
       BIN(F_MAX, fmaxf(a, bb))
       BIN(F_MIN, fminf(a, bb))
-      BIN(F_POW, call_pow(a, bb))
-      UN(F_LOG, call_log(a))
+      case OP_FN + F_POW: {  // pow(|a|, b): one inlined powf body applied to
+        float b[K], r[K], a[K];  // the K points by register rotation (static
+        POP(b);                  // indices, no K-fold code duplication)
+        FOR_K a[k] = tos[k];
+#pragma unroll 1
+        for (int it = 0; it < K; ++it) {
+          const float v = powf(fabsf(a[0]), b[0]);
+          const float b0 = b[0];
+#pragma unroll
+          for (int k = 0; k < K - 1; ++k) {
+            a[k] = a[k + 1];
+            b[k] = b[k + 1];
+          }
+          a[K - 1] = v;
+          b[K - 1] = b0;
+        }
+        FOR_K RES(k) = a[k];
+        MODI_FIN(b)
+        (void)r;
+        break;
+      }
+      UN(F_LOG, fabsf(a) > kDelta ? logf(fabsf(a)) : 0.0f)
       UN(F_EXP, expf(a))
-      UN(F_TANH, call_tanh(a))
+      UN(F_TANH, tanhf(a))
       UN(F_NEG, -a)
       UN(F_ABS, fabsf(a))
-      UN(F_SQRT, __fsqrt_rn(fabsf(a)))
-      UN(F_INV, fabsf(a) > kDelta ? __frcp_rn(a) : 0.0f)
+      case OP_FN + F_SQRT: {  // sqrt(|a|)
+        float r[K];
+        float mx = 0.0f;
+        uint32_t mn = 0xFFFFFFFFu;  // zero excluded, as in DIV
+        FOR_K {
+          mx = fmaxf(mx, fabsf(tos[k]));
+          mn = min(mn, (__float_as_uint(tos[k]) & 0x7FFFFFFFu) - 1u);
+        }
+        if constexpr (COLD) {
+          FOR_K {
+            const float a = fabsf(tos[k]);
+            RES(k) = a == 0.0f ? 0.0f
+                               : ((a <= kSqrtRange && a >= kSqrtRangeMin) ? sqrt_fast(a) : slow_sqrt(a));
+          }
+        } else {
+          bail |= !(mx <= kSqrtRange) || mn < __float_as_uint(kSqrtRangeMin) - 1u;
+          FOR_K {
+            const float a = fabsf(tos[k]);
+            RES(k) = a == 0.0f ? 0.0f : sqrt_fast(a);
+          }
+        }
+        MODI_FIN(tos)
+        (void)r;
+        break;
+      }
+      case OP_FN + F_INV: {  // |a| > delta ? 1 / a : 0
+        float r[K];
+        float mx = 0.0f;
+        FOR_K mx = fmaxf(mx, fabsf(tos[k]));
+        if constexpr (COLD) {
+          FOR_K {
+            const float a = tos[k];
+            RES(k) = fabsf(a) > kDelta ? (fabsf(a) <= kSqrtRange ? rcp_fast(a) : slow_rcp(a)) : 0.0f;
+          }
+        } else {
+          bail |= !(mx <= kSqrtRange);
+          FOR_K RES(k) = fabsf(tos[k]) > kDelta ? rcp_fast(tos[k]) : 0.0f;
+        }
+        MODI_FIN(tos)
+        (void)r;
+        break;
+      }
       BIN(F_LT, a < bb ? 1.0f : 0.0f)
       BIN(F_GT, a > bb ? 1.0f : 0.0f)
       BIN(F_LE, a <= bb ? 1.0f : 0.0f)
       BIN(F_GE, a >= bb ? 1.0f : 0.0f)
       default: {  // F_IF (ternary): a = tos, b = first pop, c = second pop
+        float b[K], c[K], r[K];
         POP(b);
         POP(c);
         FOR_K RES(k) = tos[k] > 0.0f ? b[k] : c[k];
+        MODI_FIN(c)
+        (void)r;
         break;
       }
     }
@@ -327,27 +435,11 @@ __device__ __forceinline__ void interpret(const Node* __restrict__ tree, int len
 #undef POP
 #undef BIN
 #undef UN
-#undef TRIG
-    if constexpr (MULTI) {
-      const uint32_t slot = (nd.x >> 8) & 0xFFu;
-      if (slot != kNoSlot) {
-        float* acc = accl + slot * SLOT;
-        float av[K];
-        vld<K>(acc, av);
-        FOR_K av[k] = __fadd_rn(av[k], r[k]);
-        vst<K>(acc, av);
-        // pass the rightmost child's value upward (unary: the child itself)
-        const int ar = func_arity(static_cast<int>(op) - OP_FN);
-        if (ar == 2) {
-          FOR_K tos[k] = b[k];
-        } else if (ar == 3) {
-          FOR_K tos[k] = c[k];
-        }
-      } else {
-        FOR_K tos[k] = r[k];
-      }
-    }
+#undef UN_RANGED
+#undef MODI_FIN
+    if (!COLD && bail) break;  // this lane's result is discarded; stop early
   }
+  return bail;
 }
 
 // ------------------------------------------------------------------------
@@ -373,21 +465,38 @@ __device__ __forceinline__ void deep_release(const KParams& p, int slot, int lan
   }
 }
 
-// Evaluate `tree` on one chunk with whichever stack storage the row needs.
+template <int K>
+__device__ __forceinline__ void zero_acc(float* s_acc_l, int n_out) {
+  float z[K];
+  FOR_K z[k] = 0.f;
+  for (int o = 0; o < n_out; ++o) vst<K>(s_acc_l + o * (32 * K), z);
+}
+
+// Evaluate `tree` on one chunk: the hot copy (shared-memory stack, no calls)
+// unless the row is deeper than the shared slots; a chunk in which any lane
+// left a fast path's range is re-run on the cold copy.
 template <int K, bool MULTI>
 __device__ __forceinline__ void run_chunk(const KParams& p, const Node* tree, const TreeInfo& ti, int64_t chunk_base,
                                           int lane, float* s_stack_l, float* s_acc_l, float (&tos)[K]) {
   constexpr int V = Lay<K>::V;
   const float* xl = p.xs + chunk_base + lane * V;
-  const bool deep = ti.maxdepth - 1 > p.SD;
-  int slot = 0;
-  float* stk = s_stack_l;
-  if (deep) {
-    slot = deep_acquire(p, lane);
-    stk = p.deep + static_cast<int64_t>(slot) * p.deep_slot_floats + lane * V;
+  if (MULTI) zero_acc<K>(s_acc_l, p.n_out);
+  if (ti.maxdepth - 1 <= p.SD) {
+    const bool bail = interpret<K, MULTI, false>(tree, ti.len, xl, s_stack_l, s_acc_l, tos);
+    if (__any_sync(FULL_MASK, bail)) {
+      if (lane == 0) atomicAdd(&p.ctl->cold_chunks, 1u);
+      if (MULTI) {
+        __syncwarp();
+        zero_acc<K>(s_acc_l, p.n_out);
+      }
+      interpret<K, MULTI, true>(tree, ti.len, xl, s_stack_l, s_acc_l, tos);
+    }
+  } else {
+    const int slot = deep_acquire(p, lane);
+    interpret<K, MULTI, true>(tree, ti.len, xl, p.deep + static_cast<int64_t>(slot) * p.deep_slot_floats + lane * V,
+                              s_acc_l, tos);
+    deep_release(p, slot, lane);
   }
-  interpret<K, MULTI>(tree, ti.len, xl, stk, s_acc_l, tos);
-  if (deep) deep_release(p, slot, lane);
 }
 
 // ------------------------------------------------------------------------
@@ -497,6 +606,7 @@ __global__ void k_stage_x(const float* __restrict__ X, int32_t x_layout, const f
   if (t0 == 0) {
     ctl->work = 0;
     ctl->deep = 0;
+    ctl->cold_chunks = 0;
   }
 }
 
@@ -536,11 +646,7 @@ __global__ void __launch_bounds__(32 * kInterWarps) k_inter(const KParams p) {
     }
     const int64_t chunk_base = static_cast<int64_t>(c) * (32 * K);
     float tos[K];
-    if (MODE == MODE_EVALN) {
-      float z[K];
-      FOR_K z[k] = 0.f;
-      for (int o = 0; o < p.n_out; ++o) vst<K>(s_acc_l + o * (32 * K), z);
-    }
+    if (MODE == MODE_EVALN && !ti.valid) zero_acc<K>(s_acc_l, p.n_out);
     if (ti.valid) run_chunk<K, MODE == MODE_EVALN>(p, s_tree, ti, chunk_base, lane, s_stack_l, s_acc_l, tos);
     if (MODE == MODE_EVAL1) {
       store_out1<K>(p, tp, chunk_base, lane, tos, ti.valid);
@@ -648,11 +754,7 @@ __global__ void __launch_bounds__(32 * kIntraWarps) k_intra(const KParams p) {
     for (int c = c_begin + warp; c < c_end; c += kIntraWarps) {
       const int64_t chunk_base = static_cast<int64_t>(c) * (32 * K);
       float tos[K];
-      if (MODE == MODE_EVALN) {
-        float z[K];
-        FOR_K z[k] = 0.f;
-        for (int o = 0; o < p.n_out; ++o) vst<K>(s_acc_l + o * (32 * K), z);
-      }
+      if (MODE == MODE_EVALN && !ti.valid) zero_acc<K>(s_acc_l, p.n_out);
       if (ti.valid) run_chunk<K, MODE == MODE_EVALN>(p, s_tree, ti, chunk_base, lane, s_stack_l, s_acc_l, tos);
       if (MODE == MODE_EVAL1) {
         store_out1<K>(p, tp, chunk_base, lane, tos, ti.valid);
