@@ -24,6 +24,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -52,14 +53,19 @@ __device__ __forceinline__ bool decode_node(int16_t t, float v, int n_in, int n_
     ar = 0;
     ok = ok && !modi && slot == 0;
   } else if (kind == 1) {
-    const bool in_range = floorf(v) == v && v >= 0.f && v < static_cast<float>(n_in);
+    // integrality without FRND/F2I (XU pipe): for 0 <= v < 2^23, v + 2^23 is
+    // exact iff v is an integer, and its low mantissa bits are that integer
+    const float t = __fadd_rn(v, 8388608.0f);
+    const int iv = __float_as_int(t) - 0x4B000000;
+    const bool in_range = v >= 0.f && v < static_cast<float>(n_in) && __fsub_rn(t, 8388608.0f) == v;
     nd.w0 = OP_VAR | (kNoSlot << 8);
-    nd.w1 = in_range ? static_cast<uint32_t>(static_cast<int64_t>(v) * Dpad) : 0u;
+    nd.w1 = in_range ? static_cast<uint32_t>(static_cast<int64_t>(iv) * Dpad) : 0u;
     ar = 0;
     ok = ok && !modi && slot == 0 && in_range;
   } else {
-    const bool known = floorf(v) == v && v >= 0.f && v < static_cast<float>(kNumFuncs);
-    const int f = known ? static_cast<int>(v) : 0;
+    const float t = __fadd_rn(v, 8388608.0f);
+    const bool known = v >= 0.f && v < static_cast<float>(kNumFuncs) && __fsub_rn(t, 8388608.0f) == v;
+    const int f = known ? __float_as_int(t) - 0x4B000000 : 0;
     ar = kind <= 4 ? static_cast<int>(kind) - 1 : 0;
     ok = ok && known && func_arity(f) == ar;
     if (modi) ok = ok && n_out > 1 && static_cast<int>(slot) < n_out;
@@ -323,11 +329,10 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
         // fast path: |a|, |b| <= 2^60 and a == 0 or |a| >= 2^-60; "|a| - 1ulp"
         // as an unsigned integer makes 0 wrap to the top, so one unsigned min
         // catches only the tiny non-zero a
-        float mx = 0.0f;
-        uint32_t mn = 0xFFFFFFFFu;
+        float mx = 0.0f, mn = kDivRange;
         FOR_K {
           mx = fmaxf(mx, fmaxf(fabsf(tos[k]), fabsf(b[k])));
-          mn = min(mn, (__float_as_uint(tos[k]) & 0x7FFFFFFFu) - 1u);
+          mn = fminf(mn, fabsf(tos[k]));
         }
         if constexpr (COLD) {
           FOR_K {
@@ -337,7 +342,10 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
             RES(k) = fabsf(bb) > kDelta ? (fast ? div_fast(a, bb) : slow_div(a, bb)) : 1.0f;
           }
         } else {
-          bail |= !(mx <= kDivRange) || mn < __float_as_uint(kDivRangeMin) - 1u;
+          bail |= !(mx <= kDivRange);
+          if (mn < kDivRangeMin) {  // rare: tiny or zero a — zero is fine, tiny non-zero is not
+            FOR_K bail |= tos[k] != 0.0f && fabsf(tos[k]) < kDivRangeMin;
+          }
           FOR_K RES(k) = fabsf(b[k]) > kDelta ? div_fast(tos[k], b[k]) : 1.0f;
         }
         MODI_FIN(b)
@@ -491,6 +499,21 @@ __device__ __forceinline__ void run_chunk(const KParams& p, const Node* tree, co
       }
       interpret<K, MULTI, true>(tree, ti.len, xl, s_stack_l, s_acc_l, tos);
     }
+  } else if (K == 8 && !MULTI && ti.maxdepth - 1 <= 2 * p.SD) {
+    // Too deep for K=8 slots: two K=4 passes over the same shared region hold
+    // twice the slots. The K=4 point layout is exactly group g of K=8's, so
+    // pass g yields tos[4g .. 4g+3] — the same values as a K=8 run.
+#pragma unroll
+    for (int g = 0; g < K / 4; ++g) {
+      float t4[4];
+      const bool bail = interpret<4, false, false>(tree, ti.len, xl + g * 128, s_stack_l, s_acc_l, t4);
+      if (__any_sync(FULL_MASK, bail)) {
+        if (lane == 0) atomicAdd(&p.ctl->cold_chunks, 1u);
+        interpret<4, false, true>(tree, ti.len, xl + g * 128, s_stack_l, s_acc_l, t4);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) tos[(4 * g + k) % K] = t4[k];
+    }
   } else {
     const int slot = deep_acquire(p, lane);
     interpret<K, MULTI, true>(tree, ti.len, xl, p.deep + static_cast<int64_t>(slot) * p.deep_slot_floats + lane * V,
@@ -544,11 +567,18 @@ __device__ __forceinline__ double lane_sse(const KParams& p, int64_t chunk_base,
   float yv[K];
   vld_nc<K>(p.xs + static_cast<int64_t>(p.n_in) * p.Dpad + chunk_base + lane * V, yv);
   double s = 0.0;
-  FOR_K {
-    const int64_t d = chunk_base + Lay<K>::point(lane, k);
-    if (d < p.D) {
+  if (chunk_base + 32 * K <= p.D) {  // full chunk (warp-uniform): no per-point bounds
+    FOR_K {
       const double r = static_cast<double>(v[k]) - static_cast<double>(yv[k]);
-      s = __dadd_rn(s, __dmul_rn(r, r));
+      s = fma(r, r, s);
+    }
+  } else {
+    const int rem = static_cast<int>(p.D - chunk_base);
+    FOR_K {
+      if (Lay<K>::point(lane, k) < rem) {
+        const double r = static_cast<double>(v[k]) - static_cast<double>(yv[k]);
+        s = fma(r, r, s);
+      }
     }
   }
   return s;
@@ -565,13 +595,15 @@ __device__ __forceinline__ void combine_partial(const KParams& p, int64_t tp, in
   int last = 0;
   if (lane == 0) {
     __stcg(p.partials + tp * p.nparts + part, s);
-    __threadfence();
-    const int t = atomicAdd(p.counters + tp, 1);
+    // release: the partial above is visible before the ticket; acquire: the
+    // last arriver sees every other unit's partial (no full MEMBAR.GPU)
+    int t;
+    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(t) : "l"(p.counters + tp) : "memory");
     last = (t == p.nparts - 1);
   }
   last = __shfl_sync(FULL_MASK, last, 0);
   if (!last) return;
-  __threadfence();
+  __syncwarp();  // memory ordering: lane 0's acquire happens-before the other lanes' reads
   double acc = 0.0;
   for (int q = lane; q < p.nparts; q += 32) acc += __ldcg(p.partials + tp * p.nparts + q);
   acc = warp_sum_d(acc);  // fixed lane-strided order, then a fixed shuffle tree
@@ -888,6 +920,14 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   int K;
   if (strategy == EVOGP_STRATEGY_INTER) K = D <= 32 ? 1 : (D <= 64 ? 2 : (D <= 128 || multi ? 4 : 8));
   else K = multi ? 4 : 8;
+  // tuning knobs for the calibration sweeps: datapoints
+  // per lane and the resident-warps target that sizes the shared-memory stack
+  if (const char* e = std::getenv("EVOGP_TUNE_K")) {
+    const int k = std::atoi(e);
+    if ((k == 4 || k == 8) && (strategy == EVOGP_STRATEGY_INTRA || 32 * k <= std::max<int64_t>(D, 128))) K = k;
+  }
+  int target_warps = 24;  // measured optimum for K=8 (profiles/sweep_kw_r01.txt)
+  if (const char* e = std::getenv("EVOGP_TUNE_WARPS")) target_warps = std::max(4, std::min(64, std::atoi(e)));
   const int warps = strategy == EVOGP_STRATEGY_INTER ? kInterWarps : kIntraWarps;
   const int64_t chunk = 32 * K;
   const int64_t nch = (D + chunk - 1) / chunk;
@@ -896,8 +936,8 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   const int acc_bytes = multi ? n_out * slot_bytes : 0;
   const int depth = max_depth_bound(L);
   const int tree_bytes = static_cast<int>(round_up(static_cast<int64_t>(L + 1) * 8, 16));
-  // shared-memory budget: aim at ~20 resident warps per SM
-  const int budget_per_warp = (227 * 1024) / 20;
+  // shared-memory budget: aim at `target_warps` resident warps per SM
+  const int budget_per_warp = (227 * 1024) / target_warps;
   const int per_warp_fixed = acc_bytes + (strategy == EVOGP_STRATEGY_INTER ? tree_bytes : 0);
   int SD = (budget_per_warp - per_warp_fixed) / slot_bytes;
   SD = std::max(2, std::min(SD, std::max(1, depth - 1)));
