@@ -7,7 +7,7 @@ LIB := $(PKG)/libevogp.so
 NVFLAGS := -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
            -ftz=false -prec-div=true -prec-sqrt=true -Xcompiler -fPIC,-O2 -Xptxas -v
 SRCS := $(CSRC)/kernels.cu $(CSRC)/capi.cu $(CSRC)/tensorize.cpp
-HDRS := $(CSRC)/evogp_internal.h include/evogp.h
+HDRS := $(CSRC)/evogp_internal.h $(CSRC)/fastmath.cuh $(CSRC)/selector_table.inc include/evogp.h
 
 all: $(LIB) oracle/liboracle.so synth/libsynth.so
 
