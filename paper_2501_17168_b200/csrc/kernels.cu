@@ -237,11 +237,11 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
       vld_nc<K>(xl + nd.w1, tos);
     }
   }
-  uint2 nxt = *reinterpret_cast<const uint2*>(tree + len - 1);
+  // (no software prefetch of the next node word: measured neutral-to-worse,
+  // its double buffer costs register moves on every iteration)
 #pragma unroll 1
   for (int i = len - 2; i >= 0; --i) {
-    const uint2 nd = nxt;
-    nxt = *reinterpret_cast<const uint2*>(tree + i);  // prefetch node i-1 (tree[0] is the pad)
+    const uint2 nd = *reinterpret_cast<const uint2*>(tree + i + 1);
     const uint32_t op = nd.x & 0xFFu;
     if (op <= OP_VAR) {  // leaf: push the old top, load the leaf
       vst<K>(top, tos);
@@ -326,9 +326,8 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
       case OP_FN + F_DIV: {  // |b| > delta ? a / b : 1
         float b[K], r[K];
         POP(b);
-        // fast path: |a|, |b| <= 2^60 and a == 0 or |a| >= 2^-60; "|a| - 1ulp"
-        // as an unsigned integer makes 0 wrap to the top, so one unsigned min
-        // catches only the tiny non-zero a
+        // fast path: |a|, |b| <= 2^60 and a == 0 or |a| >= 2^-60 (one max and
+        // one min over the K points; the rare small min is re-checked exactly)
         float mx = 0.0f, mn = kDivRange;
         FOR_K {
           mx = fmaxf(mx, fmaxf(fabsf(tos[k]), fabsf(b[k])));
