@@ -79,7 +79,8 @@ int run(int mode, const int16_t* type, const float* value, const int16_t* size, 
   kp.partials = reinterpret_cast<double*>(ws + pl.off_partials);
   kp.deep_locks = reinterpret_cast<int32_t*>(ws + pl.off_locks);
   kp.deep = reinterpret_cast<float*>(ws + pl.off_deep);
-  kp.use_tma = (ld % 8 == 0) && aligned(type, 16) && aligned(value, 16);
+  kp.prog = reinterpret_cast<Node*>(ws + pl.off_prog);
+  kp.info = reinterpret_cast<TreeMeta*>(ws + pl.off_info);
   int nl = 0;
   st = launch(pl, mode, X, x_layout, y, stream, &nl, t_ev_start, t_ev_end);
   t_last_launches = nl;

@@ -25,6 +25,11 @@ enum Func : int {
   F_EXP, F_TANH, F_NEG, F_ABS, F_SQRT, F_INV, F_LT, F_GT, F_LE, F_GE, F_IF
 };
 
+// Internal opcodes for binary nodes whose children the compile pass swapped
+// (f_R(a, b) = f(b, a)); LT/GT and LE/GE swap into each other, the symmetric
+// ops keep their code. Never valid in user input (ids >= kNumFuncs).
+enum : int { F_SUB_R = kNumFuncs, F_DIV_R, F_POW_R };
+
 // Arity per function id; kind word = 1 + arity for function nodes.
 EVOGP_HD constexpr int func_arity(int f) {
   return (f == F_SIN || f == F_COS || f == F_TAN || (f >= F_LOG && f <= F_INV)) ? 1 : (f == F_IF ? 3 : 2);
@@ -43,6 +48,13 @@ struct alignas(8) Node {
 };
 
 enum Mode : int { MODE_EVAL1 = 0, MODE_EVALN = 1, MODE_SSE = 2 };
+
+// Per-tree result of the compile pass: program length and operand-stack
+// depth, or maxdepth = -1 for a malformed row.
+struct alignas(8) TreeMeta {
+  int32_t len;
+  int32_t maxdepth;
+};
 
 // Layout of the small control block at the start of the workspace.
 struct Control {
@@ -73,14 +85,17 @@ struct KParams {
   int32_t nseg;     // intra: segments per tree
   int32_t seg_chunks;
   int32_t SD;               // shared-memory stack slots per warp
-  int32_t tree_bytes;       // decoded-tree bytes ((L + 1) nodes, 16B multiple)
+  int32_t tree_bytes;       // program-row bytes in shared memory (prog_ld node words)
   int32_t warp_smem_bytes;  // per-warp stack (+ Modi accumulator) bytes
-  int32_t raw_type_bytes;   // intra: raw type row bytes (16B multiple)
-  int32_t raw_value_bytes;  // intra: raw value row bytes (16B multiple)
-  int32_t use_tma;          // intra: rows are 16B aligned -> cp.async.bulk staging
   int32_t out_magic;        // ceil(2^32 / n_out) for the index split in the Modi store
   int32_t deep_slots;       // size of the deep-stack pool
   int64_t deep_slot_floats; // floats per deep-stack slot (depth bound x 32K)
+  // compiled programs (k_prepare): row t = (prog_ld) node words, word 0 a pad,
+  // words 1..len the decoded nodes; info[t] = {len, maxdepth or -1 if invalid}
+  Node* prog;
+  TreeMeta* info;
+  int32_t prog_ld;
+  int32_t reorder_scratch_bytes;  // k_prepare shared scratch per warp (0: no reordering)
   double* partials;
   int32_t* counters;
   Control* ctl;
@@ -96,7 +111,7 @@ struct Plan {
   size_t smem_bytes;
   KParams kp;
   // workspace layout
-  size_t off_ctl, off_xs, off_counters, off_partials, off_locks, off_deep, total;
+  size_t off_ctl, off_xs, off_counters, off_partials, off_locks, off_deep, off_prog, off_info, total;
 };
 
 // kernels.cu

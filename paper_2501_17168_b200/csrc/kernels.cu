@@ -323,60 +323,71 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
       BIN(F_ADD, __fadd_rn(a, bb))
       BIN(F_SUB, __fsub_rn(a, bb))
       BIN(F_MUL, __fmul_rn(a, bb))
-      case OP_FN + F_DIV: {  // |b| > delta ? a / b : 1
-        float b[K], r[K];
-        POP(b);
-        // fast path: |a|, |b| <= 2^60 and a == 0 or |a| >= 2^-60 (one max and
-        // one min over the K points; the rare small min is re-checked exactly)
-        float mx = 0.0f, mn = kDivRange;
-        FOR_K {
-          mx = fmaxf(mx, fmaxf(fabsf(tos[k]), fabsf(b[k])));
-          mn = fminf(mn, fabsf(tos[k]));
-        }
-        if constexpr (COLD) {
-          FOR_K {
-            const float a = tos[k], bb = b[k];
-            const bool fast = fabsf(a) <= kDivRange && fabsf(bb) <= kDivRange &&
-                              (a == 0.0f || fabsf(a) >= kDivRangeMin);
-            RES(k) = fabsf(bb) > kDelta ? (fast ? div_fast(a, bb) : slow_div(a, bb)) : 1.0f;
-          }
-        } else {
-          bail |= !(mx <= kDivRange);
-          if (mn < kDivRangeMin) {  // rare: tiny or zero a — zero is fine, tiny non-zero is not
-            FOR_K bail |= tos[k] != 0.0f && fabsf(tos[k]) < kDivRangeMin;
-          }
-          FOR_K RES(k) = fabsf(b[k]) > kDelta ? div_fast(tos[k], b[k]) : 1.0f;
-        }
-        MODI_FIN(b)
-        (void)r;
-        break;
-      }
+// protected division NUM / DEN (|DEN| > delta, else 1). Fast path: |NUM|,
+// |DEN| <= 2^60 and NUM == 0 or |NUM| >= 2^-60 (one max and one min over the
+// K points; the rare small min is re-checked exactly).
+#define DIV_CASE(OPC, NUM, DEN)                                                     \
+  case OPC: {                                                                       \
+    float b[K], r[K];                                                               \
+    POP(b);                                                                         \
+    float mx = 0.0f, mn = kDivRange;                                                \
+    FOR_K {                                                                         \
+      mx = fmaxf(mx, fmaxf(fabsf(tos[k]), fabsf(b[k])));                            \
+      mn = fminf(mn, fabsf(NUM[k]));                                                \
+    }                                                                               \
+    if constexpr (COLD) {                                                           \
+      FOR_K {                                                                       \
+        const float nu = NUM[k], de = DEN[k];                                       \
+        const bool fast = fabsf(nu) <= kDivRange && fabsf(de) <= kDivRange &&       \
+                          (nu == 0.0f || fabsf(nu) >= kDivRangeMin);                \
+        RES(k) = fabsf(de) > kDelta ? (fast ? div_fast(nu, de) : slow_div(nu, de)) : 1.0f; \
+      }                                                                             \
+    } else {                                                                        \
+      bail |= !(mx <= kDivRange);                                                   \
+      if (mn < kDivRangeMin) {                                                      \
+        FOR_K bail |= NUM[k] != 0.0f && fabsf(NUM[k]) < kDivRangeMin;               \
+      }                                                                             \
+      FOR_K RES(k) = fabsf(DEN[k]) > kDelta ? div_fast(NUM[k], DEN[k]) : 1.0f;      \
+    }                                                                               \
+    MODI_FIN(b)                                                                     \
+    (void)r;                                                                        \
+    break;                                                                          \
+  }
+      DIV_CASE(OP_FN + F_DIV, tos, b)
+      DIV_CASE(OP_FN + F_DIV_R, b, tos)  // children swapped by the compile pass
       UN_RANGED(F_SIN, kTrigReduceMax, fm_sin_fast, slow_sinf(a))
       UN_RANGED(F_COS, kTrigReduceMax, fm_cos_fast, slow_cosf(a))
       UN_RANGED(F_TAN, kTrigReduceMax, fm_tan_fast, slow_tanf(a))
       BIN(F_MAX, fmaxf(a, bb))
       BIN(F_MIN, fminf(a, bb))
-      case OP_FN + F_POW: {  // pow(|a|, b): one inlined powf body applied to
-        float b[K], r[K], a[K];  // the K points by register rotation (static
-        POP(b);                  // indices, no K-fold code duplication)
-        FOR_K a[k] = tos[k];
-#pragma unroll 1
-        for (int it = 0; it < K; ++it) {
-          const float v = powf(fabsf(a[0]), b[0]);
-          const float b0 = b[0];
-#pragma unroll
-          for (int k = 0; k < K - 1; ++k) {
-            a[k] = a[k + 1];
-            b[k] = b[k + 1];
-          }
-          a[K - 1] = v;
-          b[K - 1] = b0;
-        }
-        FOR_K RES(k) = a[k];
-        MODI_FIN(b)
-        (void)r;
-        break;
-      }
+// pow(|BASE|, EXPO): one inlined powf body applied to the K points by
+// register rotation (static indices, no K-fold code duplication)
+#define POW_CASE(OPC, BASE, EXPO)          \
+  case OPC: {                              \
+    float b[K], r[K], a[K], e[K];          \
+    POP(b);                                \
+    FOR_K {                                \
+      a[k] = BASE[k];                      \
+      e[k] = EXPO[k];                      \
+    }                                      \
+    _Pragma("unroll 1") for (int it = 0; it < K; ++it) { \
+      const float v = powf(fabsf(a[0]), e[0]); \
+      const float e0 = e[0];               \
+      _Pragma("unroll") for (int k = 0; k < K - 1; ++k) { \
+        a[k] = a[k + 1];                   \
+        e[k] = e[k + 1];                   \
+      }                                    \
+      a[K - 1] = v;                        \
+      e[K - 1] = e0;                       \
+    }                                      \
+    FOR_K RES(k) = a[k];                   \
+    MODI_FIN(b)                            \
+    (void)r;                               \
+    break;                                 \
+  }
+      POW_CASE(OP_FN + F_POW, tos, b)
+      POW_CASE(OP_FN + F_POW_R, b, tos)
+      BIN(F_SUB_R, __fsub_rn(bb, a))
       UN(F_LOG, fabsf(a) > kDelta ? logf(fabsf(a)) : 0.0f)
       UN(F_EXP, expf(a))
       UN(F_TANH, tanhf(a))
@@ -444,6 +455,8 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
 #undef UN
 #undef UN_RANGED
 #undef MODI_FIN
+#undef DIV_CASE
+#undef POW_CASE
     if (!COLD && bail) break;  // this lane's result is discarded; stop early
   }
   return bail;
@@ -615,30 +628,172 @@ __device__ __forceinline__ void combine_partial(const KParams& p, int64_t tp, in
 #define kNaN64 __longlong_as_double(0x7FF8000000000000ll)
 
 // ------------------------------------------------------------------------
-// a2: dataset staging
+// Evaluation-order optimisation (Sethi-Ullman) of a single-output program.
+// For each binary node evaluate first the child whose subtree needs the
+// deeper stack; every operation still sees exactly the same operand values,
+// so results are unchanged (only independent subtrees are reordered) — a
+// swapped node's opcode becomes f_R(a, b) = f(b, a). Stack need with the top
+// of stack in a register: leaf 1; unary = child; binary evaluated B then A:
+// max(need B, need A + 1). Lane 0 computes sizes / needs / swaps in a reverse
+// scan and the new prefix positions in a forward scan; the warp scatters.
+// Multi-output rows are never reordered (Modi sums are order-sensitive).
+// Returns the program's new maximum stack depth.
 // ------------------------------------------------------------------------
-__global__ void k_stage_x(const float* __restrict__ X, int32_t x_layout, const float* __restrict__ y, int64_t D,
-                          int32_t n_in, int64_t Dpad, float* __restrict__ xs, int32_t* __restrict__ counters,
-                          int64_t n_counters, Control* __restrict__ ctl) {
-  const int64_t rows = n_in + (y ? 1 : 0);
-  const int64_t total = rows * Dpad;
+__device__ __forceinline__ uint32_t reversed_op(uint32_t op) {
+  switch (op) {
+    case OP_FN + F_SUB: return OP_FN + F_SUB_R;
+    case OP_FN + F_DIV: return OP_FN + F_DIV_R;
+    case OP_FN + F_POW: return OP_FN + F_POW_R;
+    case OP_FN + F_LT: return OP_FN + F_GT;
+    case OP_FN + F_GT: return OP_FN + F_LT;
+    case OP_FN + F_LE: return OP_FN + F_GE;
+    case OP_FN + F_GE: return OP_FN + F_LE;
+    default: return op;  // ADD, MUL, MAX, MIN are symmetric
+  }
+}
+
+__device__ int reorder_program(const Node* s_nodes, int n, Node* row, unsigned char* scr, int L, int lane) {
+  uint16_t* sz = reinterpret_cast<uint16_t*>(scr);  // subtree size
+  uint16_t* nd = sz + L;                            // stack need
+  uint16_t* np = nd + L;                            // new prefix position
+  uint16_t* st = np + L;                            // scan stack of subtree roots
+  uint8_t* sw = reinterpret_cast<uint8_t*>(st + L); // children swapped
+  int depth = 0;
+  if (lane == 0) {
+    int top = 0;
+    for (int i = n - 1; i >= 0; --i) {
+      const uint32_t op = s_nodes[i + 1].w0 & 0xFFu;
+      const int ar = op <= OP_VAR ? 0 : func_arity(static_cast<int>(op) - OP_FN);
+      int s, q, swp = 0;
+      if (ar == 0) {
+        s = 1;
+        q = 1;
+      } else if (ar == 1) {
+        const int c = st[--top];
+        s = 1 + sz[c];
+        q = nd[c];
+      } else if (ar == 2) {
+        const int a = st[--top], b = st[--top];  // first pop = leftmost child
+        s = 1 + sz[a] + sz[b];
+        const int q_def = max(static_cast<int>(nd[b]), nd[a] + 1);  // B first (prefix order)
+        const int q_swp = max(static_cast<int>(nd[a]), nd[b] + 1);  // A first
+        swp = q_swp < q_def;
+        q = swp ? q_swp : q_def;
+      } else {
+        const int a = st[--top], b = st[--top], c = st[--top];
+        s = 1 + sz[a] + sz[b] + sz[c];
+        q = max(static_cast<int>(nd[c]), max(nd[b] + 1, nd[a] + 2));
+      }
+      sz[i] = static_cast<uint16_t>(s);
+      nd[i] = static_cast<uint16_t>(q);
+      sw[i] = static_cast<uint8_t>(swp);
+      st[top++] = static_cast<uint16_t>(i);
+    }
+    depth = nd[0];
+    np[0] = 0;
+    for (int i = 0; i < n; ++i) {  // parents precede children in prefix order
+      const uint32_t op = s_nodes[i + 1].w0 & 0xFFu;
+      if (op <= OP_VAR) continue;
+      const int ar = func_arity(static_cast<int>(op) - OP_FN);
+      const int c1 = i + 1;
+      if (ar == 1) {
+        np[c1] = np[i] + 1;
+      } else if (ar == 2) {
+        const int c2 = c1 + sz[c1];
+        if (sw[i]) {
+          np[c2] = np[i] + 1;
+          np[c1] = np[c2] + sz[c2];
+        } else {
+          np[c1] = np[i] + 1;
+          np[c2] = np[c1] + sz[c1];
+        }
+      } else {
+        const int c2 = c1 + sz[c1], c3 = c2 + sz[c2];
+        np[c1] = np[i] + 1;
+        np[c2] = np[c1] + sz[c1];
+        np[c3] = np[c2] + sz[c2];
+      }
+    }
+  }
+  __syncwarp();
+  depth = __shfl_sync(FULL_MASK, depth, 0);
+  for (int i = lane; i < n; i += 32) {
+    Node x = s_nodes[i + 1];
+    if (sw[i]) x.w0 = (x.w0 & ~0xFFu) | reversed_op(x.w0 & 0xFFu);
+    row[np[i] + 1] = x;
+  }
+  if (lane == 0) row[0] = s_nodes[0];
+  __syncwarp();
+  return depth;
+}
+
+// ------------------------------------------------------------------------
+// a2 + a4 (compile): one launch before the evaluation kernel
+//   * X (row-major or SoA) -> padded SoA rows Xs[n_in][Dpad] (+ y for the SSE)
+//   * every tree row -> its decoded program row (one warp per tree): decode,
+//     validate, stack depth; so the evaluation kernels only copy programs
+//   * clears the per-tree completion counters and the work-queue tickets
+// ------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* __restrict__ X, int32_t x_layout,
+                                                 const float* __restrict__ y, int64_t n_counters) {
+  const int64_t rows = p.n_in + (y ? 1 : 0);
+  const int64_t total = rows * p.Dpad;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  float* xs = const_cast<float*>(p.xs);
   for (int64_t e = t0; e < total; e += stride) {
-    const int64_t k = e / Dpad, d = e - k * Dpad;
+    const int64_t k = e / p.Dpad, d = e - k * p.Dpad;
     float v = 0.f;
-    if (d < D) {
-      if (k == n_in) v = y[d];
-      else v = x_layout == EVOGP_X_SOA ? X[k * D + d] : X[d * n_in + k];
+    if (d < p.D) {
+      if (k == p.n_in) v = y[d];
+      else v = x_layout == EVOGP_X_SOA ? X[k * p.D + d] : X[d * p.n_in + k];
     }
     xs[e] = v;
   }
-  for (int64_t e = t0; e < n_counters; e += stride) counters[e] = 0;
+  for (int64_t e = t0; e < n_counters; e += stride) p.counters[e] = 0;
   if (t0 == 0) {
-    ctl->work = 0;
-    ctl->deep = 0;
-    ctl->cold_chunks = 0;
+    p.ctl->work = 0;
+    p.ctl->deep = 0;
+    p.ctl->cold_chunks = 0;
   }
+  // compile: warp per tree
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = stride >> 5;
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* scratch = smem + static_cast<size_t>(threadIdx.x >> 5) * p.reorder_scratch_bytes;
+  for (int64_t tp = t0 >> 5; tp < p.P; tp += nwarps) {
+    Node* row = p.prog + tp * p.prog_ld;
+    TreeInfo ti;
+    if (p.reorder_scratch_bytes > 0) {
+      // decode into shared scratch; reorder when the row is deeper than the
+      // evaluation kernel's shared stack, else copy as is
+      Node* s_nodes = reinterpret_cast<Node*>(scratch);
+      ti = stage_tree_warp(p, tp, s_nodes, lane);
+      if (ti.valid && ti.maxdepth - 1 > p.SD) {
+        ti.maxdepth = reorder_program(s_nodes, ti.len, row, scratch + (p.L + 1) * 8, p.L, lane);
+      } else {
+        const uint2* src = reinterpret_cast<const uint2*>(s_nodes);
+        for (int i = lane; i <= ti.len; i += 32) reinterpret_cast<uint2*>(row)[i] = src[i];
+      }
+    } else {
+      ti = stage_tree_warp(p, tp, row, lane);
+    }
+    if (lane == 0) {
+      p.info[tp] = TreeMeta{ti.len, ti.valid ? ti.maxdepth : -1};
+      if (!ti.valid) atomicOr(&p.ctl->flags, 1);
+    }
+    __syncwarp();
+  }
+}
+
+// Copy a compiled program row (pad + len words) into a warp's shared buffer.
+__device__ __forceinline__ TreeInfo load_program_warp(const KParams& p, int64_t tp, Node* s_tree, int lane) {
+  const TreeMeta m = p.info[tp];
+  const uint2* src = reinterpret_cast<const uint2*>(p.prog + tp * p.prog_ld);
+  uint2* dst = reinterpret_cast<uint2*>(s_tree);
+  for (int i = lane; i <= m.len; i += 32) dst[i] = src[i];
+  __syncwarp();
+  return TreeInfo{m.len, m.maxdepth, m.maxdepth >= 0};
 }
 
 // ------------------------------------------------------------------------
@@ -671,9 +826,8 @@ __global__ void __launch_bounds__(32 * kInterWarps) k_inter(const KParams p) {
     const int c = static_cast<int>(u - tp * p.nch);
     if (tp != staged) {
       __syncwarp();
-      ti = stage_tree_warp(p, tp, s_tree, lane);
+      ti = load_program_warp(p, tp, s_tree, lane);
       staged = tp;
-      if (!ti.valid && lane == 0) atomicOr(&p.ctl->flags, 1);
     }
     const int64_t chunk_base = static_cast<int64_t>(c) * (32 * K);
     float tos[K];
@@ -710,23 +864,21 @@ __global__ void __launch_bounds__(32 * kIntraWarps) k_intra(const KParams p) {
   __shared__ long long s_item[2];
   constexpr int V = Lay<K>::V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // layout: raw type row | raw value row | decoded tree | per-warp stacks (+acc)
-  int16_t* raw_type = reinterpret_cast<int16_t*>(smem);
-  float* raw_value = reinterpret_cast<float*>(smem + p.raw_type_bytes);
-  Node* s_tree = reinterpret_cast<Node*>(smem + p.raw_type_bytes + p.raw_value_bytes);
-  unsigned char* wbase = smem + p.raw_type_bytes + p.raw_value_bytes + p.tree_bytes +
-                         static_cast<size_t>(warp) * p.warp_smem_bytes;
+  // layout: per-warp stacks (+acc) | compiled program row. (The row sits at a
+  // run-time offset: at offset 0 the compiler re-derives the shared-window base
+  // (S2UR SR_CgaCtaId ...) inside the interpreter loop on every node fetch.)
+  Node* s_tree = reinterpret_cast<Node*>(smem + static_cast<size_t>(kIntraWarps) * p.warp_smem_bytes);
+  unsigned char* wbase = smem + static_cast<size_t>(warp) * p.warp_smem_bytes;
   float* s_stack_l = reinterpret_cast<float*>(wbase) + lane * V;
   float* s_acc_l = s_stack_l + p.SD * 32 * K;
   if (threadIdx.x == 0) {
-    if (p.use_tma) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_item[0] = static_cast<long long>(atomicAdd(&p.ctl->work, 1ull));
   }
   __syncthreads();
   const long long nitems = p.P * p.nseg;
+  const uint32_t row_bytes = static_cast<uint32_t>(p.prog_ld) * 8u;  // 16-byte multiple
   uint32_t phase = 0;
   int it = 0;
   for (;;) {
@@ -734,51 +886,33 @@ __global__ void __launch_bounds__(32 * kIntraWarps) k_intra(const KParams p) {
     if (item >= nitems) break;
     const int64_t tp = item / p.nseg;
     const int seg = static_cast<int>(item - tp * p.nseg);
-    if (p.use_tma) {
-      // a4: TMA bulk copy of the row into shared memory, completion on an mbarrier
-      if (threadIdx.x == 0) {
-        s_item[(it + 1) & 1] = static_cast<long long>(atomicAdd(&p.ctl->work, 1ull));
-        const uint32_t bar = smem_u32(&mbar);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                     "r"(static_cast<uint32_t>(p.raw_type_bytes + p.raw_value_bytes))
-                     : "memory");
+    // a4: TMA bulk copy of the compiled program row into shared memory,
+    // completion signalled on an mbarrier; the row's metadata alongside
+    if (threadIdx.x == 0) {
+      s_item[(it + 1) & 1] = static_cast<long long>(atomicAdd(&p.ctl->work, 1ull));
+      const uint32_t bar = smem_u32(&mbar);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(row_bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(s_tree)),
+          "l"(p.prog + tp * p.prog_ld), "r"(row_bytes), "r"(bar)
+          : "memory");
+      const TreeMeta m = p.info[tp];
+      s_info = TreeInfo{m.len, m.maxdepth, m.maxdepth >= 0};
+      uint32_t done = 0;
+      while (!done) {
         asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(raw_type)),
-            "l"(p.type + tp * p.ld), "r"(static_cast<uint32_t>(p.raw_type_bytes)), "r"(bar)
+            "{\n .reg .pred P1;\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n selp.u32 %0, 1, 0, "
+            "P1;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(phase)
             : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(raw_value)),
-            "l"(p.value + tp * p.ld), "r"(static_cast<uint32_t>(p.raw_value_bytes)), "r"(bar)
-            : "memory");
-      }
-      if (warp == 0) {
-        uint32_t done = 0;
-        const uint32_t bar = smem_u32(&mbar);
-        while (!done) {
-          asm volatile(
-              "{\n .reg .pred P1;\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n selp.u32 %0, 1, 0, "
-              "P1;\n}\n"
-              : "=r"(done)
-              : "r"(bar), "r"(phase)
-              : "memory");
-        }
-        const TreeInfo ti = stage_tree_warp(p, tp, s_tree, lane, raw_type, raw_value);
-        if (lane == 0) s_info = ti;
-      }
-      phase ^= 1u;
-    } else {
-      if (threadIdx.x == 0) s_item[(it + 1) & 1] = static_cast<long long>(atomicAdd(&p.ctl->work, 1ull));
-      if (warp == 0) {
-        const TreeInfo ti = stage_tree_warp(p, tp, s_tree, lane);
-        if (lane == 0) s_info = ti;
       }
     }
+    phase ^= 1u;
     __syncthreads();
     const TreeInfo ti = s_info;
-    if (!ti.valid && threadIdx.x == 0 && seg == 0) atomicOr(&p.ctl->flags, 1);
     const int c_begin = seg * p.seg_chunks;
     const int c_end = min(p.nch, c_begin + p.seg_chunks);
     double lane_acc = 0.0;
@@ -839,6 +973,8 @@ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 // Upper bound on the operand-stack depth of a well-formed row of length L:
 // one entry per leaf at most, and leaves <= (2L + 1) / 3 when arity >= 2.
 inline int max_depth_bound(int L) { return std::min(L, (2 * L + 1) / 3 + 1); }
+
+constexpr int kReorderMaxLen = 256;
 
 template <int K, int MODE>
 const void* inter_fn() { return reinterpret_cast<const void*>(&k_inter<K, MODE>); }
@@ -946,7 +1082,9 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
     const int k = std::atoi(e);
     if ((k == 4 || k == 8) && (strategy == EVOGP_STRATEGY_INTRA || 32 * k <= std::max<int64_t>(D, 128))) K = k;
   }
-  int target_warps = 24;  // measured optimum for K=8 (profiles/sweep_kw_r01.txt)
+  // resident-warp target: 32 (the K=8 register limit) once the compile pass
+  // reorders deep programs; measured in profiles/sweep_kw_r01.txt
+  int target_warps = 32;
   if (const char* e = std::getenv("EVOGP_TUNE_WARPS")) target_warps = std::max(4, std::min(64, std::atoi(e)));
   const int warps = strategy == EVOGP_STRATEGY_INTER ? kInterWarps : kIntraWarps;
   const int64_t chunk = 32 * K;
@@ -955,18 +1093,17 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   const int slot_bytes = 32 * K * 4;
   const int acc_bytes = multi ? n_out * slot_bytes : 0;
   const int depth = max_depth_bound(L);
-  const int tree_bytes = static_cast<int>(round_up(static_cast<int64_t>(L + 1) * 8, 16));
+  const int prog_ld = static_cast<int>(round_up(L + 1, 2));  // node words per program row (16-byte rows)
+  const int tree_bytes = prog_ld * 8;
   // shared-memory budget: aim at `target_warps` resident warps per SM
   const int budget_per_warp = (227 * 1024) / target_warps;
   const int per_warp_fixed = acc_bytes + (strategy == EVOGP_STRATEGY_INTER ? tree_bytes : 0);
   int SD = (budget_per_warp - per_warp_fixed) / slot_bytes;
   SD = std::max(2, std::min(SD, std::max(1, depth - 1)));
   const int warp_smem = acc_bytes + SD * slot_bytes;
-  const int raw_type_bytes = strategy == EVOGP_STRATEGY_INTRA ? static_cast<int>(round_up(int64_t(L) * 2, 16)) : 0;
-  const int raw_value_bytes = strategy == EVOGP_STRATEGY_INTRA ? static_cast<int>(round_up(int64_t(L) * 4, 16)) : 0;
   const size_t smem = strategy == EVOGP_STRATEGY_INTER
                           ? static_cast<size_t>(warps) * (tree_bytes + warp_smem)
-                          : static_cast<size_t>(raw_type_bytes) + raw_value_bytes + tree_bytes +
+                          : static_cast<size_t>(tree_bytes) +
                                 static_cast<size_t>(warps) * warp_smem;
   if (smem > 227 * 1024) return EVOGP_E_UNSUPPORTED;
   if (static_cast<int64_t>(n_in + 1) * Dpad > 0xFFFFFFFFll) return EVOGP_E_UNSUPPORTED;  // u32 leaf offsets
@@ -1009,8 +1146,14 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   kp.SD = SD;
   kp.tree_bytes = tree_bytes;
   kp.warp_smem_bytes = warp_smem;
-  kp.raw_type_bytes = raw_type_bytes;
-  kp.raw_value_bytes = raw_value_bytes;
+  kp.prog_ld = prog_ld;
+  // evaluation-order optimisation in the compile pass: single-output rows of
+  // up to kReorderMaxLen nodes (shared scratch: nodes + 4 u16 arrays + flags)
+  kp.reorder_scratch_bytes =
+      (mode != MODE_EVALN && L <= kReorderMaxLen) ? static_cast<int32_t>(round_up(int64_t(L + 1) * 8 + 9 * L, 16)) : 0;
+  if (const char* e = std::getenv("EVOGP_TUNE_REORDER")) {
+    if (std::atoi(e) == 0) kp.reorder_scratch_bytes = 0;
+  }
   kp.out_magic = static_cast<int32_t>((0x100000000ull + n_out - 1) / n_out);
   kp.deep_slots = deep_slots;
   kp.deep_slot_floats = deep_slot_floats;
@@ -1028,6 +1171,10 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   off += round_up(static_cast<int64_t>(deep_slots) * 4, 256);
   pl.off_deep = off;
   off += round_up(static_cast<int64_t>(deep_slots) * per_slot, 256);
+  pl.off_prog = off;
+  off += round_up(P * prog_ld * 8, 256);
+  pl.off_info = off;
+  off += round_up(P * 8, 256);
   pl.total = off;
   return EVOGP_OK;
 }
@@ -1039,10 +1186,11 @@ int launch(Plan& pl, int mode, const float* X, int32_t x_layout, const float* y,
   int launches = 0;
   {
     const int64_t total = static_cast<int64_t>(kp.n_in + 1) * kp.Dpad;
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8));
-    k_stage_x<<<static_cast<int>(blocks), 256, 0, s>>>(X, x_layout, mode == MODE_SSE ? y : nullptr, kp.D, kp.n_in,
-                                                        kp.Dpad, const_cast<float*>(kp.xs), kp.counters,
-                                                        mode == MODE_SSE ? kp.P : 0, kp.ctl);
+    const int64_t blocks = std::max<int64_t>(
+        1, std::min<int64_t>(std::max((total + 255) / 256, (kp.P + 7) / 8), static_cast<int64_t>(148) * 16));
+    k_prepare<<<static_cast<int>(blocks), 256, 8 * kp.reorder_scratch_bytes, s>>>(kp, X, x_layout,
+                                                                                 mode == MODE_SSE ? y : nullptr,
+                                                        mode == MODE_SSE ? kp.P : 0);
     ++launches;
   }
   const void* fn = kernel_ptr(pl.strategy, pl.K, mode);

@@ -473,3 +473,29 @@ def test_ieee_fast_paths_bitexact():
         for row, name in enumerate(("div", "inv", "sqrt")):
             ok = same_bits_mod_zero(g[row], ref[row].astype(np.float64))
             assert ok.all(), (name, strategy, (~ok).sum(), X[~ok][:3], g[row][~ok][:3], ref[row][~ok][:3])
+
+
+@pytest.mark.parametrize("warps", ["48", "64"])
+def test_reordered_programs_bitexact(warps, monkeypatch):
+    """With a tiny shared-memory stack (many warps per SM) the compile pass
+    reorders most single-output programs (Sethi-Ullman, reversed opcodes
+    SUB_R/DIV_R/POW_R, LT<->GT, LE<->GE). Results must not change: IEEE mix
+    bit-identical to the oracle's FP32-faithful replay, full mix identical
+    to the default plan's output."""
+    P, L, n_in, D = 300, 127, 4, 700
+    pt, X, y = make_case(1100, P, L, n_in, D, "ieee", lo=-2.0, hi=2.0)
+    dt = to_device(pt, L, n_in)
+    t, v, s = oracle_arrays(pt, L, n_in)
+    r32 = oracle.evaluate(t, v, s, X, mode=1)[:, :, 0]
+    pf, Xf, yf = make_case(1200, P, L, n_in, D, "full")
+    dtf = to_device(pf, L, n_in)
+    ref_full = {st: gpu_eval(dtf, Xf, 1, st) for st in ("inter", "intra")}
+    monkeypatch.setenv("EVOGP_TUNE_WARPS", warps)
+    for strategy in ("inter", "intra"):
+        g = gpu_eval(dt, X, 1, strategy)[:, :, 0]
+        ok = same_bits_mod_zero(g, r32)
+        assert ok.all(), (strategy, (~ok).sum())
+        gf = gpu_eval(dtf, Xf, 1, strategy)
+        a, b = gf.astype(np.float32), ref_full[strategy]
+        same = (a == b) | (np.isnan(a) & np.isnan(b))
+        assert same.all(), (strategy, (~same).sum())
