@@ -1,15 +1,17 @@
 // kernels.cu — sm_100a kernels of the EvoGP hot path (arXiv 2501.17168).
 //
-//   k_stage_x        a2: X (row-major or SoA) -> padded SoA rows Xs[n_in][Dpad]
-//                         (+ y as row n_in for the SSE), clears the per-tree
-//                         completion counters and the work-queue tickets.
+//   k_prepare        a2 + compile: X (row-major or SoA) -> padded SoA rows
+//                         Xs[n_in][Dpad] (+ y for the SSE); every tree row ->
+//                         a decoded, validated program row (warp per tree),
+//                         deep single-output programs reordered (Sethi-Ullman);
+//                         clears the completion counters and work tickets.
 //   k_inter<K,MODE>  (a) inter-individual: one warp per (tree, chunk of 32*K
 //                         datapoints) pulled from a device work queue; the warp
-//                         stages and pre-decodes its tree into shared memory,
-//                         each lane evaluates K datapoints (PAPER §III-C
-//                         "hybrid parallelism").
+//                         copies its program into shared memory, each lane
+//                         evaluates K datapoints (PAPER §III-C "hybrid
+//                         parallelism").
 //   k_intra<K,MODE>  (b) intra-individual: one CTA per (tree, datapoint range);
-//                         the tree row is staged into shared memory by a TMA
+//                         the program row is staged into shared memory by a TMA
 //                         bulk copy (cp.async.bulk + mbarrier) and shared by all
 //                         8 warps, datapoints striped across the warps (PAPER
 //                         §III-C "data-level parallelism", shared memory
@@ -82,16 +84,14 @@ struct TreeInfo {
   bool valid;
 };
 
-// One warp stages row `tp` as pre-decoded Node words: node i goes to
-// s_tree[i + 1] (s_tree[0] is a pad the interpreter's prefetch may read).
-// Validation: with c_i = 1 - arity_i the stack size after processing node i
-// is the suffix sum d_i = sum_{j>=i} c_j; a row is well-formed iff every
-// d_i >= 1 and d_0 == 1 (P:358 evaluation never underflows, leaves the root).
-__device__ __forceinline__ TreeInfo stage_tree_warp(const KParams& p, int64_t tp, Node* s_tree, int lane,
-                                                    const int16_t* raw_type = nullptr,
-                                                    const float* raw_value = nullptr) {
-  const int16_t* trow = raw_type ? raw_type : p.type + tp * p.ld;
-  const float* vrow = raw_value ? raw_value : p.value + tp * p.ld;
+// One warp decodes row `tp` into Node words: node i goes to s_tree[i + 1]
+// (s_tree[0] is a pad). Validation: with c_i = 1 - arity_i the stack size
+// after processing node i is the suffix sum d_i = sum_{j>=i} c_j; a row is
+// well-formed iff every d_i >= 1 and d_0 == 1 (P:358 evaluation never
+// underflows and leaves exactly the root).
+__device__ __forceinline__ TreeInfo stage_tree_warp(const KParams& p, int64_t tp, Node* s_tree, int lane) {
+  const int16_t* trow = p.type + tp * p.ld;
+  const float* vrow = p.value + tp * p.ld;
   const int len0 = __ldg(p.size + tp * p.ld);
   const int len = min(max(len0, 1), p.L);
   bool ok = len0 >= 1 && len0 <= p.L;
@@ -103,8 +103,8 @@ __device__ __forceinline__ TreeInfo stage_tree_warp(const KParams& p, int64_t tp
     if (i < len) {
       Node nd;
       int ar;
-      const int16_t t = raw_type ? trow[i] : __ldg(trow + i);
-      const float v = raw_value ? vrow[i] : __ldg(vrow + i);
+      const int16_t t = __ldg(trow + i);
+      const float v = __ldg(vrow + i);
       ok = decode_node(t, v, p.n_in, p.n_out, p.Dpad, nd, ar) && ok;
       s_tree[i + 1] = nd;
       c = 1 - ar;
@@ -244,6 +244,18 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
     const uint2 nd = *reinterpret_cast<const uint2*>(tree + i + 1);
     const uint32_t op = nd.x & 0xFFu;
     if (op <= OP_VAR) {  // leaf: push the old top, load the leaf
+#ifdef EVOGP_EXP_LEAFTMP
+      float t[K];
+      if (op == OP_CONST) {
+        const float v = __uint_as_float(nd.y);
+        FOR_K t[k] = v;
+      } else {
+        vld_nc<K>(xl + nd.y, t);
+      }
+      vst<K>(top, tos);
+      top += SLOT;
+      FOR_K tos[k] = t[k];
+#else
       vst<K>(top, tos);
       top += SLOT;
       if (op == OP_CONST) {
@@ -252,6 +264,7 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
       } else {
         vld_nc<K>(xl + nd.y, tos);
       }
+#endif
       continue;
     }
     // Operands live only inside their case. Single-output: results go
