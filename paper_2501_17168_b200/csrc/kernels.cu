@@ -524,20 +524,22 @@ __device__ __forceinline__ void run_chunk(const KParams& p, const Node* tree, co
       }
       interpret<K, MULTI, true>(tree, ti.len, xl, s_stack_l, s_acc_l, tos);
     }
-  } else if (K == 8 && !MULTI && ti.maxdepth - 1 <= 2 * p.SD) {
-    // Too deep for K=8 slots: two K=4 passes over the same shared region hold
-    // twice the slots. The K=4 point layout is exactly group g of K=8's, so
-    // pass g yields tos[4g .. 4g+3] — the same values as a K=8 run.
+  } else if (K >= 8 && !MULTI && ti.maxdepth - 1 <= 2 * p.SD) {
+    // Too deep for K-point slots: two K/2 passes over the same shared region
+    // hold twice the slots. The K/2 point layout is exactly half h of the K
+    // layout (groups 2h.. of [groups][32 lanes][4]), so pass h yields
+    // tos[K/2*h .. K/2*h + K/2 - 1] — the same values as a K-point run.
+    constexpr int H = K >= 8 ? K / 2 : 4;
 #pragma unroll
-    for (int g = 0; g < K / 4; ++g) {
-      float t4[4];
-      const bool bail = interpret<4, false, false>(tree, ti.len, xl + g * 128, s_stack_l, s_acc_l, t4);
+    for (int h = 0; h < 2; ++h) {
+      float th[H];
+      const bool bail = interpret<H, false, false>(tree, ti.len, xl + h * 32 * H, s_stack_l, s_acc_l, th);
       if (__any_sync(FULL_MASK, bail)) {
         if (lane == 0) atomicAdd(&p.ctl->cold_chunks, 1u);
-        interpret<4, false, true>(tree, ti.len, xl + g * 128, s_stack_l, s_acc_l, t4);
+        interpret<H, false, true>(tree, ti.len, xl + h * 32 * H, s_stack_l, s_acc_l, th);
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) tos[(4 * g + k) % K] = t4[k];
+      for (int k = 0; k < H; ++k) tos[(H * h + k) % K] = th[k];
     }
   } else {
     const int slot = deep_acquire(p, lane);
