@@ -56,6 +56,8 @@ def _load():
             lib.oracle_eval_recursive.restype = ctypes.c_int
             lib.oracle_mse.argtypes = [vp, vp, i64, i64, vp]
             lib.oracle_mse.restype = ctypes.c_int
+            lib.oracle_accuracy.argtypes = [vp, vp, i64, i64, i32, vp]
+            lib.oracle_accuracy.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -143,6 +145,20 @@ def mse(pred, y):
     if st != OK:
         raise OracleError(st)
     return out
+
+
+def accuracy(out, labels):
+    """Classification accuracy per tree: argmax over outputs (ties -> lowest
+    class, NaN as -inf) vs labels (R15)."""
+    lib = _load()
+    out = np.ascontiguousarray(out, dtype=np.float64)
+    labels = np.ascontiguousarray(labels, dtype=np.int32)
+    P, D, n_out = out.shape
+    acc = np.zeros(P, dtype=np.float64)
+    st = lib.oracle_accuracy(_p(out), _p(labels), P, D, n_out, _p(acc))
+    if st != OK:
+        raise OracleError(st)
+    return acc
 
 
 def certified_points(v, e, robust, tol: float = TOL):

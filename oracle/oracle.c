@@ -30,6 +30,7 @@
  *                  table, brute force vs recursive interpreter, numpy float32)
  *   certificate: pinned by soundness property (FP32 replay within bound)
  *   mse: pinned (closed forms: SPEC S:405 example, Var(y)+(c-ybar)^2)
+ *   accuracy: pinned (SPEC S:407-415 examples, brute force vs numpy argmax)
  */
 #include <math.h>
 #include <stdint.h>
@@ -580,6 +581,38 @@ int oracle_mse(const double* pred, const float* y, int64_t P, int64_t D, double*
       s += r * r;
     }
     mse[p] = s / (double)D;
+  }
+  return OR_OK;
+}
+
+/* ==================================================================== */
+/*  Classification fitness (PAPER §V-D)        */
+/* ==================================================================== */
+
+/*
+ * acc[p] = (1/D) * #{d : argmax_o out[p][d][o] == labels[d]}.
+ * argmax: the first maximal class (ties -> lowest index), NaN counts as
+ * -inf (reading R15). The decision is taken on the values given, so callers
+ * pass FP32-faithful outputs when comparing with an FP32 evaluator.
+ */
+int oracle_accuracy(const double* out, const int32_t* labels, int64_t P, int64_t D, int32_t n_out, double* acc) {
+  if (P < 0 || D < 1 || n_out < 1 || !out || !labels || !acc) return OR_E_ARG;
+  for (int64_t p = 0; p < P; ++p) {
+    int64_t correct = 0;
+    for (int64_t d = 0; d < D; ++d) {
+      const double* o = out + (p * D + d) * n_out;
+      int best = 0;
+      double bv = isnan(o[0]) ? -INFINITY : o[0];
+      for (int c = 1; c < n_out; ++c) {
+        const double v = isnan(o[c]) ? -INFINITY : o[c];
+        if (v > bv) {
+          bv = v;
+          best = c;
+        }
+      }
+      if (best == labels[d]) ++correct;
+    }
+    acc[p] = (double)correct / (double)D;
   }
   return OR_OK;
 }

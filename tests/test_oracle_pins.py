@@ -349,3 +349,25 @@ def test_mse_identity_zero():
     t, v, s = _single([VAR], [2], n_in=3)
     out = oracle.evaluate(t, v, s, X)
     assert oracle.mse(out[:, :, 0], X[:, 2].copy())[0] == 0.0
+
+
+# ---------------------------------------------------------------- classification pins
+def test_accuracy_spec_examples():
+    """one-hot predictions matching labels -> 1.0; all-zero
+    predictions with all labels 0 -> argmax tie -> class 0 -> 1.0."""
+    labels = np.array([2, 0, 1, 1], np.int32)
+    onehot = np.zeros((1, 4, 3))
+    onehot[0, np.arange(4), labels] = 1.0
+    assert oracle.accuracy(onehot, labels)[0] == 1.0
+    assert oracle.accuracy(np.zeros((1, 4, 3)), np.zeros(4, np.int32))[0] == 1.0
+    assert oracle.accuracy(np.zeros((1, 4, 3)), labels)[0] == 0.25
+
+
+def test_accuracy_bruteforce_numpy_argmax():
+    """Reading R15 reduces to numpy's first-occurrence argmax once NaN -> -inf."""
+    rng = np.random.default_rng(3)
+    out = rng.integers(-2, 3, (20, 50, 5)).astype(np.float64)  # many ties
+    out[rng.random(out.shape) < 0.1] = np.nan
+    labels = rng.integers(0, 5, 50).astype(np.int32)
+    ref = (np.argmax(np.where(np.isnan(out), -np.inf, out), axis=2) == labels[None, :]).mean(axis=1)
+    np.testing.assert_array_equal(oracle.accuracy(out, labels), ref)
