@@ -22,7 +22,7 @@ from ._lib import (E_ARG, E_CUDA, E_FUNC_UNKNOWN, E_MALFORMED, E_OUT_RANGE, E_TO
 _LIB = _lib.load()
 
 __all__ = [
-    "tensorize", "eval", "sr_fitness", "sr_sse", "select_strategy", "workspace_size", "Workspace",
+    "tensorize", "eval", "sr_fitness", "sr_sse", "classification_accuracy", "select_strategy", "workspace_size", "Workspace",
     "check_device_flags", "EvogpError", "last_launch_count", "set_kernel_timing", "STRATEGIES",
 ]
 
@@ -180,6 +180,28 @@ def sr_sse(type_, value, size, X, y, strategy="auto", x_layout="rowmajor", max_l
     """Device: un-normalised sse[P] float64 for datapoint sharding."""
     return _sr(_LIB.evogp_sr_sse, "evogp_sr_sse", type_, value, size, X, y, strategy, x_layout, max_len, out,
                workspace, stream)
+
+
+def classification_accuracy(type_, value, size, X, labels, n_classes: int, strategy="auto", x_layout="rowmajor",
+                            max_len=None, out=None, workspace: Workspace | None = None, stream=None):
+    """Device: fused classification fitness accuracy[P] float64 (SURVEY §8(f)
+    NEXT-1): Modi trees with one output per class, argmax per
+    datapoint (ties -> lowest class, NaN as -inf) against int32 labels[D]."""
+    import torch
+
+    P, L, ld = _tree_args(type_, value, size, max_len)
+    lay, D, n_in = _x_args(X, x_layout)
+    if not labels.is_cuda or labels.dtype != torch.int32 or labels.numel() != D:
+        raise ValueError("labels must be an int32 CUDA tensor of length D")
+    if out is None:
+        out = torch.empty(P, dtype=torch.float64, device=X.device)
+    ws = _workspace(P, D, L, n_in, n_classes, X.device, workspace)
+    st = _LIB.evogp_classification_accuracy(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(X), D, n_in, lay,
+                                            n_classes, _vp(labels), _vp(out), STRATEGIES[strategy],
+                                            ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream, X.device))
+    if st != OK:
+        raise EvogpError(st, "evogp_classification_accuracy")
+    return out
 
 
 def select_strategy(P: int, D: int, max_len: int, n_outputs: int = 1, device: int = 0) -> str:

@@ -22,7 +22,7 @@ X_ROWMAJOR, X_SOA = 0, 1
 EXPORTS = (
     "evogp_tensorize", "evogp_workspace_size", "evogp_eval", "evogp_sr_fitness", "evogp_sr_sse",
     "evogp_select_strategy", "evogp_check_device_flags", "evogp_status_string", "evogp_last_error",
-    "evogp_last_launch_count", "evogp_set_kernel_timing",
+    "evogp_last_launch_count", "evogp_set_kernel_timing", "evogp_classification_accuracy",
 )
 
 
@@ -44,6 +44,8 @@ def load() -> ctypes.CDLL:
     lib.evogp_sr_fitness.restype = ctypes.c_int
     lib.evogp_sr_sse.argtypes = dev_args + [vp, vp, i32, vp, sz, vp]
     lib.evogp_sr_sse.restype = ctypes.c_int
+    lib.evogp_classification_accuracy.argtypes = dev_args + [i32, vp, vp, i32, vp, sz, vp]
+    lib.evogp_classification_accuracy.restype = ctypes.c_int
     lib.evogp_select_strategy.argtypes = [i64, i64, i32, i32, i32]
     lib.evogp_select_strategy.restype = ctypes.c_int
     lib.evogp_check_device_flags.argtypes = [vp, vp, vp]

@@ -102,8 +102,10 @@ extern "C" size_t evogp_workspace_size(int64_t P, int64_t D, int32_t max_len, in
   if (P < 0 || D < 1 || max_len < 1 || max_len > kMaxLenSupported || n_inputs < 1 || n_outputs < 1) return 0;
   const int dev = current_device();
   size_t best = 256;
-  const int modes[2] = {n_outputs > 1 ? MODE_EVALN : MODE_EVAL1, MODE_SSE};
-  for (int m = 0; m < (n_outputs > 1 ? 1 : 2); ++m) {
+  // every device call this shape admits: eval, plus SR fitness (n_out == 1)
+  // or classification (n_out > 1)
+  const int modes[2] = {n_outputs > 1 ? MODE_EVALN : MODE_EVAL1, n_outputs > 1 ? MODE_CLS : MODE_SSE};
+  for (int m = 0; m < 2; ++m) {
     for (int s = EVOGP_STRATEGY_INTER; s <= EVOGP_STRATEGY_INTRA; ++s) {
       Plan pl;
       if (plan_problem(pl, P, max_len, D, n_inputs, n_outputs, modes[m], s, dev) == EVOGP_OK)
@@ -148,6 +150,19 @@ extern "C" int evogp_sr_sse(const int16_t* type, const float* value, const int16
                             void* stream) {
   return sr_common(type, value, size, P, max_len, ld, X, D, n_inputs, x_layout, y, sse, 0, strategy, workspace,
                    ws_bytes, stream);
+}
+
+extern "C" int evogp_classification_accuracy(const int16_t* type, const float* value, const int16_t* size,
+                                             int64_t P, int32_t max_len, int32_t ld, const float* X, int64_t D,
+                                             int32_t n_inputs, int32_t x_layout, int32_t n_classes,
+                                             const int32_t* labels, double* accuracy, int32_t strategy,
+                                             void* workspace, size_t ws_bytes, void* stream) {
+  int st = check_common(type, value, size, P, max_len, ld, X, D, n_inputs, x_layout, n_classes, workspace);
+  if (st != EVOGP_OK) return st;
+  if (n_classes < 2) return fail(EVOGP_E_UNSUPPORTED, "classification needs n_classes >= 2 (Modi outputs)");
+  if (!labels || (P > 0 && !accuracy)) return fail(EVOGP_E_ARG, "null labels / accuracy");
+  return run(MODE_CLS, type, value, size, P, max_len, ld, X, D, n_inputs, x_layout, n_classes, nullptr,
+             reinterpret_cast<const float*>(labels), accuracy, 1, strategy, workspace, ws_bytes, stream);
 }
 
 extern "C" int evogp_select_strategy(int64_t P, int64_t D, int32_t max_len, int32_t n_outputs, int32_t device) {

@@ -47,7 +47,10 @@ struct alignas(8) Node {
   uint32_t w1;
 };
 
-enum Mode : int { MODE_EVAL1 = 0, MODE_EVALN = 1, MODE_SSE = 2 };
+enum Mode : int { MODE_EVAL1 = 0, MODE_EVALN = 1, MODE_SSE = 2, MODE_CLS = 3 };
+// Modes whose trees accumulate Modi outputs, and modes reduced to one number per tree
+EVOGP_HD constexpr bool mode_multi(int m) { return m == MODE_EVALN || m == MODE_CLS; }
+EVOGP_HD constexpr bool mode_reduce(int m) { return m == MODE_SSE || m == MODE_CLS; }
 
 // Per-tree result of the compile pass: program length and operand-stack
 // depth, or maxdepth = -1 for a malformed row.

@@ -611,6 +611,36 @@ __device__ __forceinline__ double lane_sse(const KParams& p, int64_t chunk_base,
   return s;
 }
 
+// Classification (NEXT-1): per point, the predicted class is
+// the first maximal Modi output (ties -> lowest class, NaN as -inf; reading
+// R15), compared with the label staged (as a float) in the y row. Returns the
+// lane's count of correct points.
+template <int K>
+__device__ __forceinline__ double lane_correct(const KParams& p, int64_t chunk_base, int lane, const float* acc) {
+  constexpr int V = Lay<K>::V;
+  float lab[K];
+  vld_nc<K>(p.xs + static_cast<int64_t>(p.n_in) * p.Dpad + chunk_base + lane * V, lab);
+  int correct = 0;
+  FOR_K {
+    const int pt = Lay<K>::point(lane, k);
+    if (chunk_base + pt < p.D) {
+      float best = acc[pt];
+      best = best != best ? -INFINITY : best;
+      int cls = 0;
+      for (int o = 1; o < p.n_out; ++o) {
+        float v = acc[o * (32 * K) + pt];
+        v = v != v ? -INFINITY : v;
+        if (v > best) {
+          best = v;
+          cls = o;
+        }
+      }
+      correct += static_cast<float>(cls) == lab[k];
+    }
+  }
+  return static_cast<double>(correct);
+}
+
 // Deterministic cross-unit combine of per-tree partial SSEs: every unit
 // writes its partial; the last to arrive (per-tree counter) sums all
 // partials in a fixed order and writes the result (reading R9).
@@ -750,7 +780,7 @@ __device__ int reorder_program(const Node* s_nodes, int n, Node* row, unsigned c
 //   * clears the per-tree completion counters and the work-queue tickets
 // ------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* __restrict__ X, int32_t x_layout,
-                                                 const float* __restrict__ y, int64_t n_counters) {
+                                                 const float* __restrict__ y, int y_is_label, int64_t n_counters) {
   const int64_t rows = p.n_in + (y ? 1 : 0);
   const int64_t total = rows * p.Dpad;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -760,12 +790,15 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
     const int64_t k = e / p.Dpad, d = e - k * p.Dpad;
     float v = 0.f;
     if (d < p.D) {
-      if (k == p.n_in) v = y[d];
+      if (k == p.n_in) v = y_is_label ? static_cast<float>(reinterpret_cast<const int32_t*>(y)[d]) : y[d];
       else v = x_layout == EVOGP_X_SOA ? X[k * p.D + d] : X[d * p.n_in + k];
     }
     xs[e] = v;
   }
   for (int64_t e = t0; e < n_counters; e += stride) p.counters[e] = 0;
+  // the deep-pool locks are re-zeroed every call: a workspace may be reused
+  // across plans whose section offsets differ (e.g. inter vs intra partials)
+  for (int64_t e = t0; e < p.deep_slots; e += stride) p.deep_locks[e] = 0;
   if (t0 == 0) {
     p.ctl->work = 0;
     p.ctl->deep = 0;
@@ -846,14 +879,16 @@ __global__ void __launch_bounds__(32 * kInterWarps) k_inter(const KParams p) {
     }
     const int64_t chunk_base = static_cast<int64_t>(c) * (32 * K);
     float tos[K];
-    if (MODE == MODE_EVALN && !ti.valid) zero_acc<K>(s_acc_l, p.n_out);
-    if (ti.valid) run_chunk<K, MODE == MODE_EVALN>(p, s_tree, ti, chunk_base, lane, s_stack_l, s_acc_l, tos);
+    if (mode_multi(MODE) && !ti.valid) zero_acc<K>(s_acc_l, p.n_out);
+    if (ti.valid) run_chunk<K, mode_multi(MODE)>(p, s_tree, ti, chunk_base, lane, s_stack_l, s_acc_l, tos);
     if (MODE == MODE_EVAL1) {
       store_out1<K>(p, tp, chunk_base, lane, tos, ti.valid);
     } else if (MODE == MODE_EVALN) {
       store_outn<K>(p, tp, chunk_base, lane, s_acc_l - lane * V, ti.valid);
     } else {
-      double s = ti.valid ? lane_sse<K>(p, chunk_base, lane, tos) : kNaN64;
+      double s = !ti.valid ? kNaN64
+                           : (MODE == MODE_CLS ? lane_correct<K>(p, chunk_base, lane, s_acc_l - lane * V)
+                                               : lane_sse<K>(p, chunk_base, lane, tos));
       s = warp_sum_d(s);
       combine_partial(p, tp, c, s, lane);
     }
@@ -934,23 +969,24 @@ __global__ void __launch_bounds__(32 * kIntraWarps) k_intra(const KParams p) {
     for (int c = c_begin + warp; c < c_end; c += kIntraWarps) {
       const int64_t chunk_base = static_cast<int64_t>(c) * (32 * K);
       float tos[K];
-      if (MODE == MODE_EVALN && !ti.valid) zero_acc<K>(s_acc_l, p.n_out);
-      if (ti.valid) run_chunk<K, MODE == MODE_EVALN>(p, s_tree, ti, chunk_base, lane, s_stack_l, s_acc_l, tos);
+      if (mode_multi(MODE) && !ti.valid) zero_acc<K>(s_acc_l, p.n_out);
+      if (ti.valid) run_chunk<K, mode_multi(MODE)>(p, s_tree, ti, chunk_base, lane, s_stack_l, s_acc_l, tos);
       if (MODE == MODE_EVAL1) {
         store_out1<K>(p, tp, chunk_base, lane, tos, ti.valid);
       } else if (MODE == MODE_EVALN) {
         store_outn<K>(p, tp, chunk_base, lane, s_acc_l - lane * V, ti.valid);
       } else if (ti.valid) {
-        lane_acc += lane_sse<K>(p, chunk_base, lane, tos);
+        lane_acc += MODE == MODE_CLS ? lane_correct<K>(p, chunk_base, lane, s_acc_l - lane * V)
+                                     : lane_sse<K>(p, chunk_base, lane, tos);
       }
     }
-    if (MODE == MODE_SSE) {
+    if (mode_reduce(MODE)) {
       // a7: lanes -> warp (shuffle) -> CTA (shared memory, fixed order) -> tree
       const double w = warp_sum_d(lane_acc);
       if (lane == 0) s_red[warp] = w;
     }
     __syncthreads();  // s_red complete; everyone is done with s_tree / raw rows
-    if (MODE == MODE_SSE && warp == 0) {
+    if (mode_reduce(MODE) && warp == 0) {
       double s = lane < kIntraWarps ? s_red[lane] : 0.0;
 #pragma unroll
       for (int off = 4; off > 0; off >>= 1) s += __shfl_xor_sync(FULL_MASK, s, off);
@@ -1001,6 +1037,7 @@ const void* kernel_ptr(int strategy, int K, int mode) {
   if (K == KK) {                                            \
     if (mode == MODE_EVAL1) return S##_fn<KK, MODE_EVAL1>(); \
     if (mode == MODE_EVALN) return S##_fn<KK, MODE_EVALN>(); \
+    if (mode == MODE_CLS) return S##_fn<KK, MODE_CLS>();     \
     return S##_fn<KK, MODE_SSE>();                          \
   }
   if (strategy == EVOGP_STRATEGY_INTER) {
@@ -1087,7 +1124,7 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   if (strategy == EVOGP_STRATEGY_AUTO) strategy = select_strategy(P, D, L, n_out, device);
   if (strategy != EVOGP_STRATEGY_INTER && strategy != EVOGP_STRATEGY_INTRA) return EVOGP_E_ARG;
   const int sms = num_sms(device);
-  const bool multi = mode == MODE_EVALN;
+  const bool multi = mode_multi(mode);
   int K;
   if (strategy == EVOGP_STRATEGY_INTER) K = D <= 32 ? 1 : (D <= 64 ? 2 : (D <= 128 || multi ? 4 : 8));
   else K = multi ? 4 : 8;
@@ -1165,7 +1202,7 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   // evaluation-order optimisation in the compile pass: single-output rows of
   // up to kReorderMaxLen nodes (shared scratch: nodes + 4 u16 arrays + flags)
   kp.reorder_scratch_bytes =
-      (mode != MODE_EVALN && L <= kReorderMaxLen) ? static_cast<int32_t>(round_up(int64_t(L + 1) * 8 + 9 * L, 16)) : 0;
+      (!mode_multi(mode) && L <= kReorderMaxLen) ? static_cast<int32_t>(round_up(int64_t(L + 1) * 8 + 9 * L, 16)) : 0;
   if (const char* e = std::getenv("EVOGP_TUNE_REORDER")) {
     if (std::atoi(e) == 0) kp.reorder_scratch_bytes = 0;
   }
@@ -1181,7 +1218,7 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   pl.off_counters = off;
   off += round_up(P * 4, 256);
   pl.off_partials = off;
-  off += mode == MODE_SSE && kp.nparts > 1 ? round_up(P * kp.nparts * 8, 256) : 0;
+  off += mode_reduce(mode) && kp.nparts > 1 ? round_up(P * kp.nparts * 8, 256) : 0;
   pl.off_locks = off;
   off += round_up(static_cast<int64_t>(deep_slots) * 4, 256);
   pl.off_deep = off;
@@ -1204,8 +1241,8 @@ int launch(Plan& pl, int mode, const float* X, int32_t x_layout, const float* y,
     const int64_t blocks = std::max<int64_t>(
         1, std::min<int64_t>(std::max((total + 255) / 256, (kp.P + 7) / 8), static_cast<int64_t>(148) * 16));
     k_prepare<<<static_cast<int>(blocks), 256, 8 * kp.reorder_scratch_bytes, s>>>(kp, X, x_layout,
-                                                                                 mode == MODE_SSE ? y : nullptr,
-                                                        mode == MODE_SSE ? kp.P : 0);
+                                                                                 mode_reduce(mode) ? y : nullptr,
+                                                        mode == MODE_CLS, mode_reduce(mode) ? kp.P : 0);
     ++launches;
   }
   const void* fn = kernel_ptr(pl.strategy, pl.K, mode);

@@ -279,6 +279,38 @@ def test_edge_deep_stack_spill():
         assert same_bits_mod_zero(g, r32).all(), strategy
 
 
+def test_workspace_reuse_across_plans(monkeypatch):
+    """One Workspace shared by calls whose plans lay it out differently
+    (inter vs intra partials shift the deep-pool section): stale bytes from
+    one plan must not read as held deep-pool locks in the next."""
+    evogp = _evogp()
+    monkeypatch.setenv("EVOGP_TUNE_REORDER", "0")  # keep the left combs deep -> global pool
+    L, n_in, P, D = 127, 2, 40, 5000
+    offs, tys, vas = [0], [], []
+    rng = np.random.default_rng(6)
+    for _ in range(P):
+        tys += [1] * 63 + [1] * 64
+        vas += list(rng.integers(0, 2, 127).astype(np.float32))
+        offs.append(len(tys))
+    for i in range(P):  # left comb of additions (type 3 = function, value 0 = ADD)
+        tys[offs[i]:offs[i] + 63] = [3] * 63
+        vas[offs[i]:offs[i] + 63] = [0.0] * 63
+    pt = synth.PrefixTrees(np.array(offs, np.int64), np.array(tys, np.int16), np.array(vas, np.float32))
+    X = synth.dataset_X(10, 0, D, n_in, lo=0.5, hi=1.5)
+    y = synth.pagie_y(X)
+    t, v, s = to_device(pt, L, n_in)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    ws = evogp.Workspace(P, D, L, n_in, 1, Xd.device)
+    r = oracle.evaluate(*oracle_arrays(pt, L, n_in), X, mode=1)[:, :, 0]
+    ref = oracle.mse(r, y)
+    for strategy in ("inter", "intra", "inter", "intra"):
+        m = evogp.sr_fitness(t, v, s, Xd, yd, strategy=strategy, workspace=ws)
+        g = evogp.eval(t, v, s, Xd, strategy=strategy, workspace=ws)
+        torch.cuda.synchronize()
+        assert same_bits_mod_zero(g.cpu().numpy()[:, :, 0], r).all(), strategy
+        assert np.allclose(m.cpu().numpy(), ref, rtol=1e-9), strategy
+
+
 def test_edge_malformed_row_nan_and_flag():
     evogp = _evogp()
     pt, X, y = make_case(900, 20, 15, 2, 64, "paper")
@@ -499,3 +531,88 @@ def test_reordered_programs_bitexact(warps, monkeypatch):
         a, b = gf.astype(np.float32), ref_full[strategy]
         same = (a == b) | (np.isnan(a) & np.isnan(b))
         assert same.all(), (strategy, (~same).sum())
+
+
+# ---------------------------------------------------------------- NEXT-1: classification fitness
+def gpu_acc(dev_trees, X, labels, n_classes, strategy, L=None):
+    evogp = _evogp()
+    t, v, s = dev_trees
+    a = evogp.classification_accuracy(t, v, s, torch.from_numpy(X).cuda(), torch.from_numpy(labels).cuda(),
+                                      n_classes, strategy=strategy, max_len=L)
+    torch.cuda.synchronize()
+    return a.cpu().numpy()
+
+
+def _labels(seed, D, n_classes):
+    # synthetic class labels incl. a few out-of-range ones (never match, R15)
+    rng = np.random.default_rng(seed)
+    lab = rng.integers(0, n_classes, size=D).astype(np.int32)
+    lab[rng.random(D) < 0.01] = -1
+    lab[rng.random(D) < 0.01] = n_classes
+    return lab
+
+
+@pytest.mark.parametrize("strategy", ["inter", "intra"])
+@pytest.mark.parametrize("P,L,n_in,n_cls,D", [(200, 63, 17, 6, 4096), (64, 31, 4, 2, 1000), (33, 127, 8, 3, 20_001)])
+def test_classification_ieee_exact(strategy, P, L, n_in, n_cls, D):
+    """IEEE mix: outputs are FP32-faithful bit-exact (Tier A), so every argmax
+    decision and the accuracy must equal the oracle's exactly."""
+    pt, X, _ = make_case(900 + D, P, L, n_in, D, "ieee", n_out=n_cls, modi=0.1, dist="normal")
+    lab = _labels(D, D, n_cls)
+    dt = to_device(pt, L, n_in, n_cls)
+    a = gpu_acc(dt, X, lab, n_cls, strategy)
+    t, v, s = oracle_arrays(pt, L, n_in, n_cls)
+    r32 = oracle.evaluate(t, v, s, X, n_out=n_cls, mode=1)
+    ref = oracle.accuracy(r32, lab)
+    np.testing.assert_array_equal(np.rint(a * D), np.rint(ref * D))
+    assert np.abs(a - ref).max() <= 1e-15
+    assert 0.0 < ref.mean() < 1.0
+
+
+@pytest.mark.parametrize("mix", ["paper", "full"])
+def test_classification_self_consistent_and_kernels_agree(mix):
+    """Any mix: the fused accuracy equals the oracle argmax applied to the GPU's
+    own eval outputs (the fusion adds no arithmetic), and (a) == (b)."""
+    P, L, n_in, n_cls, D = 300, 63, 17, 5, 5000
+    pt, X, _ = make_case(950, P, L, n_in, D, mix, n_out=n_cls, modi=0.1, dist="normal")
+    lab = _labels(7, D, n_cls)
+    dt = to_device(pt, L, n_in, n_cls)
+    g = gpu_eval(dt, X, n_cls, "inter").astype(np.float64)
+    ref = oracle.accuracy(g, lab)
+    for strategy in ("inter", "intra", "auto"):
+        a = gpu_acc(dt, X, lab, n_cls, strategy)
+        np.testing.assert_array_equal(np.rint(a * D), np.rint(ref * D))
+
+
+def test_classification_edge_cases():
+    evogp = _evogp()
+    # single tree, single point; three-class Modi tree from the golden Fig. 6 case
+    import json
+    import os
+
+    from tests.conftest import GOLDEN
+
+    g = json.load(open(os.path.join(GOLDEN, "fig6_modi_tree.json")))
+    pt = synth.PrefixTrees(np.array([0, 13], np.int64), np.array(g["types"], np.int16),
+                           np.array(g["values"], np.float32))
+    dt = to_device(pt, 13, 5, 3)
+    X = np.array([[g["inputs"][k] for k in "abcde"]], np.float32)
+    want = int(np.argmax(np.array(g["expected_outputs"], np.float64)))
+    for strategy in ("inter", "intra"):
+        for c in range(3):
+            a = gpu_acc(dt, X, np.array([c], np.int32), 3, strategy)
+            assert a[0] == (1.0 if c == want else 0.0)
+    # n_classes < 2 is rejected loudly
+    t, v, s = dt
+    with pytest.raises(evogp.EvogpError):
+        evogp.classification_accuracy(t, v, s, torch.from_numpy(X).cuda(), torch.zeros(1, dtype=torch.int32,
+                                      device="cuda"), 1)
+    # ties -> lowest class: a lone constant leaf writes no Modi slot, so both
+    # outputs are 0 and the prediction is class 0 (R15)
+    pt = synth.PrefixTrees(np.array([0, 1], np.int64), np.array([0], np.int16), np.array([2.5], np.float32))
+    dt = to_device(pt, 1, 1, 2)
+    X = np.zeros((37, 1), np.float32)
+    np.testing.assert_array_equal(gpu_eval(dt, X, 2, "inter"), 0.0)
+    for strategy in ("inter", "intra"):
+        assert gpu_acc(dt, X, np.zeros(37, np.int32), 2, strategy)[0] == 1.0
+        assert gpu_acc(dt, X, np.ones(37, np.int32), 2, strategy)[0] == 0.0
