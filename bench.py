@@ -165,6 +165,9 @@ def oracle_pass(pt, cfg, X, y, threads):
     import oracle
 
     t, v, s = oracle.tensorize(pt.offsets, pt.types, pt.values, cfg.max_len, cfg.n_in, cfg.n_out)
+    if cfg.paired:
+        oracle.evaluate_paired(t, v, s, X.reshape(t.shape[0], cfg.D, cfg.n_in), n_out=cfg.n_out, mode=0)
+        return
     out = oracle.evaluate(t, v, s, X, n_out=cfg.n_out, mode=0, threads=threads)
     if cfg.n_out == 1:
         oracle.mse(out[:, :, 0], y)
@@ -176,10 +179,14 @@ def oracle_sample(cfg, mix, target_work=4e8):
     D = min(cfg.D, 1 << 16)
     per_tree = 0.75 * cfg.max_len * D
     n = int(max(1, min(cfg.P, target_work // per_tree)))
+    if cfg.paired:  # the oracle walks one individual at a time: a smaller sample
+        n = min(n, 20_000)
     pt = synth.trees(cfg.seed, 0, n, cfg.max_len, synth.MIXES[mix], cfg.n_in, cfg.n_out, cfg.modi_prob)
-    X, y = synth.config_data(cfg, 0, D)
+    X, y = synth.config_data(cfg, 0, n * cfg.D if cfg.paired else D)
     nodes = int(np.diff(pt.offsets).sum())
     desc = f"first {n} of {cfg.P} trees x first {D} of {cfg.D} datapoints ({nodes * D:.3e} node*dp per pass)"
+    if cfg.paired:
+        desc = f"first {n} of {cfg.P} individuals, each on its own {cfg.D} observation(s) ({nodes * D:.3e} node*obs)"
     return pt, X, y, nodes * D, desc
 
 
@@ -248,20 +255,34 @@ def main():
 
     axis, (p0, p1), (d0, d1) = local_shards(cfg, rank, world)
     pt = synth.trees(cfg.seed, p0, p1 - p0, cfg.max_len, synth.MIXES[mix], cfg.n_in, cfg.n_out, cfg.modi_prob)
-    X, y = synth.config_data(cfg, d0, d1 - d0)
+    if cfg.paired:  # NEXT-2: every individual's own B observations, rows p0*B ...
+        X, y = synth.config_data(cfg, p0 * cfg.D, (p1 - p0) * cfg.D)
+        X = X.reshape(p1 - p0, cfg.D, cfg.n_in) if cfg.D > 1 else X
+    else:
+        X, y = synth.config_data(cfg, d0, d1 - d0)
     nodes, sfu_frac = tree_stats(pt)
     t, v, s = evogp.tensorize(pt.offsets, pt.types, pt.values, cfg.max_len, cfg.n_in, cfg.n_out)
     td, vd, sd = (torch.from_numpy(a).to(dev) for a in (t, v, s))
     Xd, yd = torch.from_numpy(X).to(dev), torch.from_numpy(y).to(dev)
     P_local, D_local = p1 - p0, d1 - d0
     strategy = args.strategy
-    chosen = evogp.select_strategy(P_local, D_local, cfg.max_len, cfg.n_out, local) if strategy == "auto" else strategy
+    if cfg.paired:
+        chosen = "paired"
+    else:
+        chosen = (evogp.select_strategy(P_local, D_local, cfg.max_len, cfg.n_out, local) if strategy == "auto"
+                  else strategy)
     ws = evogp.Workspace(P_local, D_local, cfg.max_len, cfg.n_in, cfg.n_out, device=dev)
     out_eval = torch.empty((P_local, D_local, cfg.n_out), dtype=torch.float32, device=dev) if cfg.n_out > 1 else None
+    if cfg.paired:
+        out_eval = torch.empty(((P_local, cfg.n_out) if cfg.D == 1 else (P_local, cfg.D, cfg.n_out)),
+                               dtype=torch.float32, device=dev)
     mse_local = torch.full((P_local,), float("nan"), dtype=torch.float64, device=dev)
     P_total = cfg.P * world if axis == "pop" else cfg.P
 
     def step():
+        if cfg.paired:
+            evogp.eval_paired(td, vd, sd, Xd, n_outputs=cfg.n_out, out=out_eval, workspace=ws)
+            return out_eval
         if cfg.n_out > 1:
             evogp.eval(td, vd, sd, Xd, n_outputs=cfg.n_out, strategy=strategy, out=out_eval, workspace=ws)
             return out_eval
@@ -369,6 +390,13 @@ def main():
         roof = 1.0 / max(1.0 / r_fp32, sfu_frac / r_sfu)  # per GPU
         per_launch_work = float(nodes) * D_local  # rank 0's units per launch
         achieved = per_launch_work * args.steps / (kern_ms * 1e-3)
+        if cfg.paired:
+            # NEXT-2 is a single streaming pass: bound by HBM. Algorithmic bytes
+            # per launch: type+value of every node (6 B), size[0] per row, the
+            # observations and the outputs
+            alg_bytes = 6.0 * nodes + 2.0 * P_local + 4.0 * P_local * cfg.D * (cfg.n_in + cfg.n_out)
+            hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+            gbs = alg_bytes * args.steps / (kern_ms * 1e-3) / 1e9
         traffic = None
         prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_{chosen}_summary.json")
         if os.path.exists(prof):
@@ -385,12 +413,19 @@ def main():
                        "strategy": chosen, "parallelism": f"{axis}-shard x{world}",
                        "cold_rerun_chunks_last_step": cold_chunks,
                        "l2": "flushed (256 MiB write) before every timed step",
-                       "step": ("evogp_eval" if cfg.n_out > 1 else "evogp_sr_fitness") +
+                       "step": ("evogp_eval_paired" if cfg.paired else
+                                "evogp_eval" if cfg.n_out > 1 else "evogp_sr_fitness") +
                                (" + NCCL combine" if world > 1 else "")},
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": roof, "unit": UNIT, "frac": achieved / roof,
-                         "traffic": traffic, "kernel": f"k_{chosen}",
-                         "peak_basis": f"{SMS} SMs x min({FP32_LANES} FP32, {SFU_LANES}/s MUFU) lanes/clk at "
-                                       f"sm_max_mhz={f / 1e6:.0f} ({peak_src}), s={sfu_frac:.3f}"},
+            "roofline": ({"bound": "alu", "achieved": achieved, "peak": roof, "unit": UNIT, "frac": achieved / roof,
+                          "traffic": traffic, "kernel": f"k_{chosen}",
+                          "peak_basis": f"{SMS} SMs x min({FP32_LANES} FP32, {SFU_LANES}/s MUFU) lanes/clk at "
+                                        f"sm_max_mhz={f / 1e6:.0f} ({peak_src}), s={sfu_frac:.3f}"}
+                         if not cfg.paired else
+                         {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+                          "traffic": traffic, "kernel": "k_paired", "algorithmic_bytes_per_launch": alg_bytes,
+                          "alu_view": {"achieved": achieved, "unit": UNIT, "fp32_sfu_roof": roof,
+                                       "frac": achieved / roof},
+                          "peak_basis": f"hbm_gbs ({peak_src})"}),
             "gpu_launches": launches,
             "clocks": clocks,
             "e2e": e2e,

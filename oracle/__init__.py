@@ -133,6 +133,19 @@ def evaluate_recursive(types, values, x, n_out: int = 1, mode: int = 0):
     return out
 
 
+def evaluate_paired(type_, value, size, obs, n_out: int = 1, mode: int = 0):
+    """Paired per-individual inference (PAPER §III-C, SURVEY §8(f)
+    NEXT-2): tree p evaluated on its own observations obs[p] ([P,B,n_in]).
+    Row by row through `evaluate`. Returns out[P,B,n_out] float64."""
+    obs = np.asarray(obs, dtype=np.float32)
+    P, B, _ = obs.shape
+    out = np.zeros((P, B, n_out), dtype=np.float64)
+    for p in range(P):
+        out[p] = evaluate(type_[p:p + 1], value[p:p + 1], size[p:p + 1], obs[p], n_out=n_out, mode=mode,
+                          threads=1)[0]
+    return out
+
+
 def mse(pred, y):
     """mse[p] = mean_d (pred[p,d] - y[d])^2 in FP64 (reading R7)."""
     lib = _load()

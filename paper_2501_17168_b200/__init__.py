@@ -22,7 +22,7 @@ from ._lib import (E_ARG, E_CUDA, E_FUNC_UNKNOWN, E_MALFORMED, E_OUT_RANGE, E_TO
 _LIB = _lib.load()
 
 __all__ = [
-    "tensorize", "eval", "sr_fitness", "sr_sse", "classification_accuracy", "select_strategy", "workspace_size", "Workspace",
+    "tensorize", "eval", "sr_fitness", "sr_sse", "classification_accuracy", "eval_paired", "select_strategy", "workspace_size", "Workspace",
     "check_device_flags", "EvogpError", "last_launch_count", "set_kernel_timing", "STRATEGIES",
 ]
 
@@ -202,6 +202,40 @@ def classification_accuracy(type_, value, size, X, labels, n_classes: int, strat
     if st != OK:
         raise EvogpError(st, "evogp_classification_accuracy")
     return out
+
+
+def eval_paired(type_, value, size, obs, n_outputs: int = 1, max_len=None, out=None,
+                workspace: Workspace | None = None, stream=None):
+    """Device: paired per-individual inference (PAPER
+    P:346): tree p evaluated on its own observations obs[p] ([P, n_in] or
+    [P, B, n_in] float32) -> out [P, n_outputs] or [P, B, n_outputs]."""
+    import torch
+
+    P, L, ld = _tree_args(type_, value, size, max_len)
+    if not obs.is_cuda or obs.dtype != torch.float32 or not obs.is_contiguous() or obs.dim() not in (2, 3):
+        raise ValueError("obs must be a contiguous float32 CUDA tensor [P, n_in] or [P, B, n_in]")
+    if obs.shape[0] != P:
+        raise ValueError("obs.shape[0] must equal the population size")
+    B = 1 if obs.dim() == 2 else int(obs.shape[1])
+    n_in = int(obs.shape[-1])
+    shape = (P, n_outputs) if obs.dim() == 2 else (P, B, n_outputs)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.float32, device=obs.device)
+    ws = workspace if workspace is not None else _flags_workspace(obs.device)
+    st = _LIB.evogp_eval_paired(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(obs), B, n_in, n_outputs,
+                                _vp(out), ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream, obs.device))
+    if st != OK:
+        raise EvogpError(st, "evogp_eval_paired")
+    return out
+
+
+def _flags_workspace(device):
+    key = ("flags", str(device))
+    w = _WS_CACHE.get(key)
+    if w is None:
+        w = Workspace(1, 1, 1, 1, 1, device)
+        _WS_CACHE[key] = w
+    return w
 
 
 def select_strategy(P: int, D: int, max_len: int, n_outputs: int = 1, device: int = 0) -> str:

@@ -23,6 +23,7 @@ EXPORTS = (
     "evogp_tensorize", "evogp_workspace_size", "evogp_eval", "evogp_sr_fitness", "evogp_sr_sse",
     "evogp_select_strategy", "evogp_check_device_flags", "evogp_status_string", "evogp_last_error",
     "evogp_last_launch_count", "evogp_set_kernel_timing", "evogp_classification_accuracy",
+    "evogp_eval_paired",
 )
 
 
@@ -46,6 +47,8 @@ def load() -> ctypes.CDLL:
     lib.evogp_sr_sse.restype = ctypes.c_int
     lib.evogp_classification_accuracy.argtypes = dev_args + [i32, vp, vp, i32, vp, sz, vp]
     lib.evogp_classification_accuracy.restype = ctypes.c_int
+    lib.evogp_eval_paired.argtypes = [vp, vp, vp, i64, i32, i32, vp, i32, i32, i32, vp, vp, sz, vp]
+    lib.evogp_eval_paired.restype = ctypes.c_int
     lib.evogp_select_strategy.argtypes = [i64, i64, i32, i32, i32]
     lib.evogp_select_strategy.restype = ctypes.c_int
     lib.evogp_check_device_flags.argtypes = [vp, vp, vp]

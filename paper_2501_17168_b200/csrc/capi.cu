@@ -165,6 +165,26 @@ extern "C" int evogp_classification_accuracy(const int16_t* type, const float* v
              reinterpret_cast<const float*>(labels), accuracy, 1, strategy, workspace, ws_bytes, stream);
 }
 
+extern "C" int evogp_eval_paired(const int16_t* type, const float* value, const int16_t* size, int64_t P,
+                                 int32_t max_len, int32_t ld, const float* obs, int32_t B, int32_t n_inputs,
+                                 int32_t n_outputs, float* out, void* workspace, size_t ws_bytes, void* stream) {
+  t_last_launches = 0;
+  if (B < 1) return fail(EVOGP_E_ARG, "B < 1");
+  // an empty population may come with an empty (null) observation array
+  static const float kNoObs = 0.0f;
+  int st = check_common(type, value, size, P, max_len, ld, P == 0 && !obs ? &kNoObs : obs, B, n_inputs,
+                        EVOGP_X_ROWMAJOR, n_outputs, workspace);
+  if (st != EVOGP_OK) return st;
+  if (P > 0 && !out) return fail(EVOGP_E_ARG, "null out");
+  if (ws_bytes < 256) return fail(EVOGP_E_ARG, "workspace too small: paired inference needs 256 bytes");
+  if (P > (int64_t(1) << 40) / B) return fail(EVOGP_E_ARG, "P * B out of range");
+  int nl = 0;
+  st = launch_paired(type, value, size, P, max_len, ld, obs, B, n_inputs, n_outputs, out, workspace, stream, &nl,
+                     t_ev_start, t_ev_end);
+  t_last_launches = nl;
+  return st;
+}
+
 extern "C" int evogp_select_strategy(int64_t P, int64_t D, int32_t max_len, int32_t n_outputs, int32_t device) {
   if (P < 0 || D < 1 || max_len < 1 || n_outputs < 1) return EVOGP_E_ARG;
   return select_strategy(P, D, max_len, n_outputs, device);

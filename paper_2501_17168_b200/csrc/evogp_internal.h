@@ -18,6 +18,12 @@ constexpr int kNumFuncs = 22;
 constexpr int kMaxLenSupported = 8192;
 constexpr int kMaxInputs = 4096;
 constexpr int kMaxOutputs = 256;
+constexpr float kDelta = 0.001f;  // protection threshold (reading R3)
+
+// Upper bound on the operand-stack depth of a well-formed row of <= L nodes
+// (arities <= 3): with d_i the stack size after node i (reverse order),
+// d_i <= #suffix nodes and d_i <= 2*#prefix nodes + 1, so d <= (2L+1)/3.
+EVOGP_HD constexpr int max_depth_bound(int L) { return L < (2 * L + 1) / 3 + 1 ? L : (2 * L + 1) / 3 + 1; }
 
 // Function ids (include/evogp.h, reading R3)
 enum Func : int {
@@ -123,6 +129,11 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
 int launch(Plan& pl, int mode, const float* X, int32_t x_layout, const float* y, void* stream, int* n_launches,
            void* ev_start = nullptr, void* ev_end = nullptr);
 int select_strategy(int64_t P, int64_t D, int32_t L, int32_t n_out, int device);
+
+// paired.cu
+int launch_paired(const int16_t* type, const float* value, const int16_t* size, int64_t P, int32_t L, int32_t ld,
+                  const float* obs, int32_t B, int32_t n_in, int32_t n_out, float* out, void* ctl, void* stream,
+                  int* n_launches, void* ev_start = nullptr, void* ev_end = nullptr);
 
 void set_last_error(const char* msg);
 

@@ -128,6 +128,7 @@ class Config:
     x_hi: float
     modi_prob: float
     index: int
+    paired: bool = False  # NEXT-2: D = observations per individual (B), each tree on its own
 
     @property
     def seed(self) -> int:
@@ -140,6 +141,9 @@ CONFIGS = {
     "c3": Config("c3_intra", 1000, 127, 8, 1, 1 << 20, "uniform", -1.0, 1.0, 0.0, 3),
     "c4": Config("c4_large_pop", 1_000_000, 127, 8, 1, 256, "uniform", -1.0, 1.0, 0.0, 4),
     "c5": Config("c5_multi_output", 10_000, 63, 17, 6, 4096, "normal", 0.0, 0.0, 0.1, 5),
+    # NEXT-2: one control step of 10^6 policy trees, each on
+    # its own 17-dim observation, 6 Modi outputs (shapes from config 5)
+    "n2": Config("n2_paired_policy", 1_000_000, 63, 17, 6, 1, "normal", 0.0, 0.0, 0.1, 6, True),
 }
 
 

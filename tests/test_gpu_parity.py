@@ -616,3 +616,82 @@ def test_classification_edge_cases():
     for strategy in ("inter", "intra"):
         assert gpu_acc(dt, X, np.zeros(37, np.int32), 2, strategy)[0] == 1.0
         assert gpu_acc(dt, X, np.ones(37, np.int32), 2, strategy)[0] == 0.0
+
+
+# ---------------------------------------------------------------- NEXT-2: paired per-individual inference
+def gpu_paired(dev_trees, obs, n_out, L=None):
+    evogp = _evogp()
+    t, v, s = dev_trees
+    o = evogp.eval_paired(t, v, s, torch.from_numpy(np.ascontiguousarray(obs)).cuda(), n_outputs=n_out, max_len=L)
+    torch.cuda.synchronize()
+    return o.cpu().numpy()
+
+
+@pytest.mark.parametrize("P,L,n_in,n_out,B", [(1000, 63, 17, 6, 1), (333, 31, 4, 1, 1), (257, 127, 8, 1, 3),
+                                              (70, 63, 17, 6, 5), (5, 15, 2, 1, 1)])
+def test_paired_ieee_bitexact(P, L, n_in, n_out, B):
+    pt, _, _ = make_case(1100 + P, P, L, n_in, 1, "ieee", n_out=n_out, modi=0.1 if n_out > 1 else 0.0)
+    obs = synth.dataset_X(1100 + P, 1, P * B, n_in, "normal", -2.0, 2.0).reshape(P, B, n_in)
+    dt = to_device(pt, L, n_in, n_out)
+    g = gpu_paired(dt, obs, n_out)
+    t, v, s = oracle_arrays(pt, L, n_in, n_out)
+    r32 = oracle.evaluate_paired(t, v, s, obs, n_out=n_out, mode=1)
+    ok = same_bits_mod_zero(g, r32)
+    assert ok.all(), (~ok).sum()
+    # 2-D obs ([P, n_in]) is the B = 1 case
+    if B == 1:
+        g2 = gpu_paired(dt, obs[:, 0, :], n_out)
+        assert g2.shape == (P, n_out)
+        assert np.array_equal(g2.view(np.uint32), g[:, 0, :].view(np.uint32))
+
+
+@pytest.mark.parametrize("mix,n_out", [("full", 1), ("paper", 1), ("full", 6)])
+def test_paired_equals_eval_on_same_points(mix, n_out):
+    """Paired inference computes what evogp_eval computes: tree p at obs[p][b]
+    equals eval's out[p][d] for the same point (bit-exact modulo +-0), on any mix."""
+    P, L, n_in, D, B = 400, 63, 17, 64, 2
+    pt, X, _ = make_case(1200, P, L, n_in, D, mix, n_out=n_out, modi=0.1 if n_out > 1 else 0.0, dist="normal")
+    dt = to_device(pt, L, n_in, n_out)
+    full = gpu_eval(dt, X, n_out, "inter")
+    idx = np.random.default_rng(3).integers(0, D, size=(P, B))
+    obs = X[idx]  # [P, B, n_in]
+    g = gpu_paired(dt, obs, n_out)
+    want = np.take_along_axis(full, idx[:, :, None], axis=1)
+    ok = same_bits_mod_zero(g, want.astype(np.float64))
+    assert ok.all(), (~ok).sum()
+    # and against the FP64 oracle on certified points
+    t, v, s = oracle_arrays(pt, L, n_in, n_out)
+    r64 = oracle.evaluate_paired(t, v, s, obs, n_out=n_out, mode=0)
+    lit = oracle.within_tol(g, r64)
+    assert lit.mean() > 0.9
+
+
+def test_paired_edge_cases():
+    evogp = _evogp()
+    # deep left comb (stack depth 64 at L = 127) and a malformed row
+    L, n_in = 127, 2
+    offs, tys, vas = [0], [], []
+    for _ in range(3):
+        tys += [3] * 63 + [1] * 64
+        vas += [0.0] * 63 + [0.0, 1.0] * 32
+        offs.append(len(tys))
+    pt = synth.PrefixTrees(np.array(offs, np.int64), np.array(tys, np.int16), np.array(vas, np.float32))
+    obs = np.array([[1.0, 2.0], [0.5, 0.25], [-1.0, 3.0]], np.float32)
+    t, v, s = evogp.tensorize(pt.offsets, pt.types, pt.values, L, n_in, 1)
+    s = s.copy()
+    s[2, 0] = 5  # row 2 claims 5 nodes: not a well-formed prefix
+    dev = [torch.from_numpy(a).cuda() for a in (t, v, s)]
+    ws = evogp.Workspace(3, 1, L, n_in, 1, "cuda")
+    o = evogp.eval_paired(*dev, torch.from_numpy(obs).cuda(), workspace=ws).cpu().numpy()
+    np.testing.assert_array_equal(o[:2, 0], [32 * 1.0 + 32 * 2.0, 32 * 0.5 + 32 * 0.25])
+    assert np.isnan(o[2, 0])
+    assert evogp.check_device_flags(ws) & 1
+    # empty population
+    e = [torch.empty((0, L), dtype=d, device="cuda") for d in (torch.int16, torch.float32, torch.int16)]
+    assert evogp.eval_paired(*e, torch.empty((0, n_in), device="cuda")).shape == (0, 1)
+    # a max_len whose stack cannot fit in shared memory is rejected, not truncated
+    big = 8192
+    tb = torch.full((1, big), -1, dtype=torch.int16, device="cuda")
+    with pytest.raises(evogp.EvogpError):
+        evogp.eval_paired(tb, torch.zeros((1, big), device="cuda"), torch.zeros((1, big), dtype=torch.int16,
+                          device="cuda"), torch.zeros((1, n_in), device="cuda"))

@@ -371,3 +371,22 @@ def test_accuracy_bruteforce_numpy_argmax():
     labels = rng.integers(0, 5, 50).astype(np.int32)
     ref = (np.argmax(np.where(np.isnan(out), -np.inf, out), axis=2) == labels[None, :]).mean(axis=1)
     np.testing.assert_array_equal(oracle.accuracy(out, labels), ref)
+
+
+# ---------------------------------------------------------------- paired inference (NEXT-2)
+@pytest.mark.parametrize("n_out,modi", [(1, 0.0), (3, 0.2)])
+def test_paired_equals_recursive_per_individual(n_out, modi):
+    """evaluate_paired (each individual on its own observation) ==
+    the independent recursive interpreter applied to tree p at obs[p][b]."""
+    P, L, n_in, B = 25, 15, 3, 2
+    pt = synth.trees(41, 0, P, L, synth.MIXES["full"], n_in, n_out, modi)
+    t, v, s = oracle.tensorize(pt.offsets, pt.types, pt.values, L, n_in, n_out)
+    obs = synth.dataset_X(41, 1, P * B, n_in, "normal", -1.0, 1.0).reshape(P, B, n_in)
+    for mode in (0, 1):
+        out = oracle.evaluate_paired(t, v, s, obs, n_out=n_out, mode=mode)
+        for p in range(P):
+            tys, vas = pt.types[pt.offsets[p]:pt.offsets[p + 1]], pt.values[pt.offsets[p]:pt.offsets[p + 1]]
+            for b in range(B):
+                r = oracle.evaluate_recursive(tys, vas, obs[p, b], n_out=n_out, mode=mode)
+                same = (out[p, b] == r) | (np.isnan(out[p, b]) & np.isnan(r))
+                assert same.all(), (p, b, out[p, b], r)
