@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 
 #include "decode.cuh"
@@ -71,6 +72,38 @@ __device__ __forceinline__ float apply_fn(int f, float a, float b, float c) {
   }
 }
 
+// A backward-moving register window over one row: the aligned 16-byte block
+// holding node i is loaded once and serves the next 8 types / 4 values, so a
+// lane issues ~3 loads per 8 nodes instead of 2 per node. (A 16-byte-aligned
+// block that holds a valid byte never leaves the allocation's pages.)
+struct RowWindow {
+  const unsigned char* tbase;
+  const unsigned char* vbase;
+  uint4 tw;
+  float4 vw;
+  int t_lo, v_lo;  // node index held in half 0 of tw / word 0 of vw
+
+  __device__ __forceinline__ int16_t type(int i) {
+    if (i < t_lo) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(tbase + 2 * i);
+      tw = __ldg(reinterpret_cast<const uint4*>(a & ~uintptr_t(15)));
+      t_lo = i - static_cast<int>((a & 15) >> 1);
+    }
+    const int k = i - t_lo;
+    const uint32_t w = (k & 4) ? ((k & 2) ? tw.w : tw.z) : ((k & 2) ? tw.y : tw.x);
+    return static_cast<int16_t>((k & 1) ? (w >> 16) : (w & 0xFFFFu));
+  }
+  __device__ __forceinline__ float value(int i) {
+    if (i < v_lo) {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(vbase + 4 * i);
+      vw = __ldg(reinterpret_cast<const float4*>(a & ~uintptr_t(15)));
+      v_lo = i - static_cast<int>((a & 15) >> 2);
+    }
+    const int k = i - v_lo;
+    return (k & 2) ? ((k & 1) ? vw.w : vw.z) : ((k & 1) ? vw.y : vw.x);
+  }
+};
+
 struct PairedParams {
   const int16_t* type;
   const float* value;
@@ -106,11 +139,13 @@ __global__ void __launch_bounds__(32 * kPairedWarps) k_paired(const PairedParams
       for (int o = 0; o < q.n_out; ++o) acc[o * 32] = 0.0f;
     int d = 0;  // operand-stack size (top in `tos`, the rest in stk[0 .. d-2])
     float tos = 0.0f;
+    RowWindow win{reinterpret_cast<const unsigned char*>(trow), reinterpret_cast<const unsigned char*>(vrow),
+                  make_uint4(0, 0, 0, 0), make_float4(0.f, 0.f, 0.f, 0.f), INT_MAX, INT_MAX};
 #pragma unroll 1
     for (int i = len - 1; i >= 0 && ok; --i) {
       Node nd;
       int ar;
-      ok = decode_node(__ldg(trow + i), __ldg(vrow + i), q.n_in, q.n_out, 1, nd, ar);
+      ok = decode_node(win.type(i), win.value(i), q.n_in, q.n_out, 1, nd, ar);
       const uint32_t op = nd.w0 & 0xFFu;
       if (!ok) break;
       if (op <= OP_VAR) {
