@@ -48,6 +48,11 @@ EVOGP_HD constexpr int func_arity(int f) {
 //     SoA dataset (index * Dpad), so a leaf needs no multiply at run time.
 enum : uint32_t { OP_CONST = 0, OP_VAR = 1, OP_FN = 2 };
 constexpr uint32_t kNoSlot = 0xFF;
+// Leaf fusion (compile pass, single-output programs): w0 bit 16 = the node
+// absorbed its first child, a leaf whose payload is w1; bit 17 = that leaf is
+// a VAR (w1 = its X offset), else a CONST (w1 = its bits).
+constexpr uint32_t kFuse = 1u << 16;
+constexpr uint32_t kFuseVar = 1u << 17;
 struct alignas(8) Node {
   uint32_t w0;
   uint32_t w1;
@@ -104,7 +109,8 @@ struct KParams {
   Node* prog;
   TreeMeta* info;
   int32_t prog_ld;
-  int32_t reorder_scratch_bytes;  // k_prepare shared scratch per warp (0: no reordering)
+  int32_t reorder_scratch_bytes;  // k_prepare shared scratch per warp (0: no reordering / fusion)
+  int32_t fuse;                   // leaf fusion on (single-output programs with scratch)
   double* partials;
   int32_t* counters;
   Control* ctl;

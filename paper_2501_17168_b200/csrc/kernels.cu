@@ -251,10 +251,32 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
 #define POP(v)   \
   top -= SLOT;   \
   vld<K>(top, v)
+// fused leaf operand (compile-pass leaf fusion; never set in MULTI programs)
+#define LEAF_OPERAND(v)                              \
+  if (nd.x & kFuseVar) {                             \
+    vld_nc<K>(xl + nd.y, v);                         \
+  } else {                                           \
+    const float cv = __uint_as_float(nd.y);          \
+    FOR_K v[k] = cv;                                 \
+  }
+// operand b: the fused leaf, else the first pop
+#define POPB(v)                                      \
+  if (!MULTI && (nd.x & kFuse)) {                    \
+    LEAF_OPERAND(v)                                  \
+  } else {                                           \
+    POP(v);                                          \
+  }
+// unary on a fused leaf: push the old top, the leaf becomes the operand
+#define UNPRE                                        \
+  if (!MULTI && (nd.x & kFuse)) {                    \
+    vst<K>(top, tos);                                \
+    top += SLOT;                                     \
+    LEAF_OPERAND(tos)                                \
+  }
 #define BIN(F, EXPR)                     \
   case OP_FN + F: {                      \
     float b[K], r[K];                    \
-    POP(b);                              \
+    POPB(b)                              \
     FOR_K {                              \
       const float a = tos[k], bb = b[k]; \
       RES(k) = (EXPR);                   \
@@ -265,6 +287,7 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
   }
 #define UN(F, EXPR)           \
   case OP_FN + F: {           \
+    UNPRE                     \
     float r[K];               \
     FOR_K {                   \
       const float a = tos[k]; \
@@ -277,6 +300,7 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
 // range-checked unary: one check per node (max |x| over the K points)
 #define UN_RANGED(F, OK_MAX, FAST, SLOW_EXPR)                    \
   case OP_FN + F: {                                              \
+    UNPRE                                                        \
     float r[K];                                                  \
     float m = 0.0f;                                              \
     FOR_K m = fmaxf(m, fabsf(tos[k]));                           \
@@ -304,7 +328,7 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
 #define DIV_CASE(OPC, NUM, DEN)                                                     \
   case OPC: {                                                                       \
     float b[K], r[K];                                                               \
-    POP(b);                                                                         \
+    POPB(b)                                                                         \
     float mx = 0.0f, mn = kDivRange;                                                \
     FOR_K {                                                                         \
       mx = fmaxf(mx, fmaxf(fabsf(tos[k]), fabsf(b[k])));                            \
@@ -340,7 +364,7 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
 #define POW_CASE(OPC, BASE, EXPO)          \
   case OPC: {                              \
     float b[K], r[K], a[K], e[K];          \
-    POP(b);                                \
+    POPB(b)                                \
     FOR_K {                                \
       a[k] = BASE[k];                      \
       e[k] = EXPO[k];                      \
@@ -369,6 +393,7 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
       UN(F_NEG, -a)
       UN(F_ABS, fabsf(a))
       case OP_FN + F_SQRT: {  // sqrt(|a|)
+        UNPRE
         float r[K];
         float mx = 0.0f;
         uint32_t mn = 0xFFFFFFFFu;  // zero excluded, as in DIV
@@ -394,6 +419,7 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
         break;
       }
       case OP_FN + F_INV: {  // |a| > delta ? 1 / a : 0
+        UNPRE
         float r[K];
         float mx = 0.0f;
         FOR_K mx = fmaxf(mx, fabsf(tos[k]));
@@ -426,6 +452,9 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
     }
 #undef RES
 #undef POP
+#undef POPB
+#undef UNPRE
+#undef LEAF_OPERAND
 #undef BIN
 #undef UN
 #undef UN_RANGED
@@ -651,6 +680,9 @@ __device__ __forceinline__ uint32_t reversed_op(uint32_t op) {
     case OP_FN + F_SUB: return OP_FN + F_SUB_R;
     case OP_FN + F_DIV: return OP_FN + F_DIV_R;
     case OP_FN + F_POW: return OP_FN + F_POW_R;
+    case OP_FN + F_SUB_R: return OP_FN + F_SUB;
+    case OP_FN + F_DIV_R: return OP_FN + F_DIV;
+    case OP_FN + F_POW_R: return OP_FN + F_POW;
     case OP_FN + F_LT: return OP_FN + F_GT;
     case OP_FN + F_GT: return OP_FN + F_LT;
     case OP_FN + F_LE: return OP_FN + F_GE;
@@ -659,7 +691,7 @@ __device__ __forceinline__ uint32_t reversed_op(uint32_t op) {
   }
 }
 
-__device__ int reorder_program(const Node* s_nodes, int n, Node* row, unsigned char* scr, int L, int lane) {
+__device__ int reorder_program(const Node* s_nodes, int n, Node* row, unsigned char* scr, int L, int lane) {  // row: shared or global
   uint16_t* sz = reinterpret_cast<uint16_t*>(scr);  // subtree size
   uint16_t* nd = sz + L;                            // stack need
   uint16_t* np = nd + L;                            // new prefix position
@@ -734,6 +766,46 @@ __device__ int reorder_program(const Node* s_nodes, int n, Node* row, unsigned c
   return depth;
 }
 
+// Leaf fusion: a unary/binary node whose first child (the next node in
+// prefix order) is a leaf absorbs that leaf — its payload moves into w1 and
+// the flags kFuse / kFuseVar are set. The interpreter then computes a binary
+// f(leaf, top) as f_R(top, leaf) (the leaf is operand b: no push, no pop) and
+// a unary f(leaf) by pushing the old top and applying f to the leaf: the same
+// operations on the same operands, one dispatch fewer per absorbed leaf. The
+// last node (the first one evaluated) is never absorbed. Warp-parallel:
+// decisions are local, positions come from a ballot prefix count.
+__device__ int fuse_copy(const Node* prog, int n, Node* row, int lane) {
+  int carry = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    bool keep = false;
+    Node y{0u, 0u};
+    if (i < n) {
+      y = prog[i + 1];
+      const uint32_t op = y.w0 & 0xFFu;
+      const bool absorbed = op <= OP_VAR && i >= 1 && i != n - 1 && (prog[i].w0 & 0xFFu) >= OP_FN &&
+                            func_arity(static_cast<int>(prog[i].w0 & 0xFFu) - OP_FN) <= 2;
+      keep = !absorbed;
+      if (keep && op >= OP_FN && i + 1 < n - 1) {
+        const int ar = func_arity(static_cast<int>(op) - OP_FN);
+        const Node leaf = prog[i + 2];
+        const uint32_t lop = leaf.w0 & 0xFFu;
+        if (ar <= 2 && lop <= OP_VAR) {
+          const uint32_t fop = ar == 2 ? reversed_op(op) : op;
+          y.w0 = (y.w0 & ~0xFFu) | fop | kFuse | (lop == OP_VAR ? kFuseVar : 0u);
+          y.w1 = leaf.w1;
+        }
+      }
+    }
+    const unsigned m = __ballot_sync(FULL_MASK, keep);
+    if (keep) row[carry + __popc(m & ((1u << lane) - 1u)) + 1] = y;
+    carry += __popc(m);
+  }
+  if (lane == 0) row[0] = prog[0];
+  __syncwarp();
+  return carry;
+}
+
 // ------------------------------------------------------------------------
 // a2 + a4 (compile): one launch before the evaluation kernel
 //   * X (row-major or SoA) -> padded SoA rows Xs[n_in][Dpad] (+ y for the SSE)
@@ -776,14 +848,21 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
     TreeInfo ti;
     if (p.reorder_scratch_bytes > 0) {
       // decode into shared scratch; reorder when the row is deeper than the
-      // evaluation kernel's shared stack, else copy as is
+      // evaluation kernel's shared stack; then fuse leaves while copying out
       Node* s_nodes = reinterpret_cast<Node*>(scratch);
+      Node* s_reord = s_nodes + (p.L + 1);
       ti = stage_tree_warp(p, tp, s_nodes, lane);
+      const Node* prog = s_nodes;
       if (ti.valid && ti.maxdepth - 1 > p.SD) {
-        ti.maxdepth = reorder_program(s_nodes, ti.len, row, scratch + (p.L + 1) * 8, p.L, lane);
+        ti.maxdepth = reorder_program(s_nodes, ti.len, s_reord, scratch + 2 * (p.L + 1) * 8, p.L, lane);
+        prog = s_reord;
+      }
+      if (ti.valid && p.fuse) {
+        ti.len = fuse_copy(prog, ti.len, row, lane);
       } else {
-        const uint2* src = reinterpret_cast<const uint2*>(s_nodes);
+        const uint2* src = reinterpret_cast<const uint2*>(prog);
         for (int i = lane; i <= ti.len; i += 32) reinterpret_cast<uint2*>(row)[i] = src[i];
+        __syncwarp();
       }
     } else {
       ti = stage_tree_warp(p, tp, row, lane);
@@ -1161,11 +1240,16 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   kp.warp_smem_bytes = warp_smem;
   kp.prog_ld = prog_ld;
   // evaluation-order optimisation in the compile pass: single-output rows of
-  // up to kReorderMaxLen nodes (shared scratch: nodes + 4 u16 arrays + flags)
+  // up to kReorderMaxLen nodes (shared scratch: nodes, reordered nodes, 4 u16 arrays + flags)
   kp.reorder_scratch_bytes =
-      (!mode_multi(mode) && L <= kReorderMaxLen) ? static_cast<int32_t>(round_up(int64_t(L + 1) * 8 + 9 * L, 16)) : 0;
+      (!mode_multi(mode) && L <= kReorderMaxLen) ? static_cast<int32_t>(round_up(int64_t(L + 1) * 16 + 9 * L, 16)) : 0;
   if (const char* e = std::getenv("EVOGP_TUNE_REORDER")) {
     if (std::atoi(e) == 0) kp.reorder_scratch_bytes = 0;
+  }
+  // leaf fusion of single-output programs (measured: profiles/fuse_ab_r01.txt)
+  kp.fuse = kp.reorder_scratch_bytes > 0 ? 1 : 0;
+  if (const char* e = std::getenv("EVOGP_TUNE_FUSE")) {
+    if (std::atoi(e) == 0) kp.fuse = 0;
   }
   kp.out_magic = static_cast<int32_t>((0x100000000ull + n_out - 1) / n_out);
   kp.deep_slots = deep_slots;
