@@ -111,6 +111,7 @@ struct KParams {
   int32_t prog_ld;
   int32_t reorder_scratch_bytes;  // k_prepare shared scratch per warp (0: no reordering / fusion)
   int32_t fuse;                   // leaf fusion on (single-output programs with scratch)
+  int32_t reorder_above;          // rows with maxdepth - 1 > this are reordered
   double* partials;
   int32_t* counters;
   Control* ctl;

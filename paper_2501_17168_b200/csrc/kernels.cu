@@ -853,7 +853,7 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
       Node* s_reord = s_nodes + (p.L + 1);
       ti = stage_tree_warp(p, tp, s_nodes, lane);
       const Node* prog = s_nodes;
-      if (ti.valid && ti.maxdepth - 1 > p.SD) {
+      if (ti.valid && ti.maxdepth - 1 > p.reorder_above) {
         ti.maxdepth = reorder_program(s_nodes, ti.len, s_reord, scratch + 2 * (p.L + 1) * 8, p.L, lane);
         prog = s_reord;
       }
@@ -1248,6 +1248,8 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   }
   // leaf fusion of single-output programs (measured: profiles/fuse_ab_r01.txt)
   kp.fuse = kp.reorder_scratch_bytes > 0 ? 1 : 0;
+  kp.reorder_above = SD;
+  if (const char* e = std::getenv("EVOGP_TUNE_REORDER_ABOVE")) kp.reorder_above = std::atoi(e) * SD;
   if (const char* e = std::getenv("EVOGP_TUNE_FUSE")) {
     if (std::atoi(e) == 0) kp.fuse = 0;
   }
