@@ -15,8 +15,8 @@ $(LIB): $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; exit 1)
 
 # test infrastructure (never linked into the product)
-oracle/liboracle.so: oracle/oracle.c
-	gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -pthread -o $@ $< -lm
+oracle/liboracle.so: oracle/oracle.c oracle/variation.c
+	gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -pthread -o $@ oracle/oracle.c oracle/variation.c -lm
 
 synth/libsynth.so: synth/synth.c
 	gcc -O2 -fPIC -shared -pthread -o $@ $< -lm

@@ -32,12 +32,12 @@ TOL = 1e-4  # north star: |gpu - oracle| <= 1e-4 * max(1, |oracle|)
 
 
 def build(force: bool = False) -> str:
-    src = os.path.join(_HERE, "oracle.c")
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
+    srcs = [os.path.join(_HERE, f) for f in ("oracle.c", "variation.c")]
+    if force or not os.path.exists(_SO) or any(os.path.getmtime(_SO) < os.path.getmtime(f) for f in srcs):
         # plain -O2, no -ffast-math, no FMA contraction: the oracle computes
-        # exactly the expressions written in oracle.c
+        # exactly the expressions written in oracle.c / variation.c
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-                               "-pthread", "-o", _SO, src, "-lm"])
+                               "-pthread", "-o", _SO] + srcs + ["-lm"])
     return _SO
 
 
@@ -58,6 +58,17 @@ def _load():
             lib.oracle_mse.restype = ctypes.c_int
             lib.oracle_accuracy.argtypes = [vp, vp, i64, i64, i32, vp]
             lib.oracle_accuracy.restype = ctypes.c_int
+            u64 = ctypes.c_uint64
+            lib.orv_draw.argtypes = [u64, u64, u64]
+            lib.orv_draw.restype = ctypes.c_uint32
+            lib.oracle_exchange.argtypes = [i64, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp]
+            lib.oracle_exchange.restype = ctypes.c_int
+            lib.oracle_tournament.argtypes = [vp, i64, i32, i64, u64, i32, vp]
+            lib.oracle_tournament.restype = ctypes.c_int
+            lib.oracle_generate.argtypes = [i64, vp, u64, vp, vp, vp]
+            lib.oracle_generate.restype = ctypes.c_int
+            lib.oracle_reproduce.argtypes = [vp, vp, vp, i64, i32, vp, i64, vp, u64, vp, vp, vp, vp, vp]
+            lib.oracle_reproduce.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -202,3 +213,104 @@ def within_tol(gpu, ref, tol: float = TOL):
     with np.errstate(invalid="ignore", over="ignore"):
         close = np.abs(gpu - ref) <= tol * np.maximum(1.0, np.abs(ref))
     return same_nan & same_inf & (~fin | close)
+
+
+# ---------------------------------------------------------------------------
+# Genetic operators (oracle/variation.c)
+# ---------------------------------------------------------------------------
+MUTATIONS = ("subtree", "hoist", "point", "multi_point", "insert", "delete", "const", "multi_const")
+PUR = dict(tour1=1, tour2=2, xo_gate=3, xo_k=4, xo_j=5, mut_gate=6, mut_kind=7, mut_site=8, point_coin=9,
+           point_new=10, gen=11)
+OP_XO, OP_XO_REJECTED, OP_MUT_NOP = 1, 2, 0x100
+
+
+class OvCfg(ctypes.Structure):
+    """Mirror of OvCfg in variation.c (DESIGN.md §14 field list)."""
+    _fields_ = [("max_len", ctypes.c_int32), ("n_inputs", ctypes.c_int32), ("n_outputs", ctypes.c_int32),
+                ("func_mask", ctypes.c_uint32), ("const_lo", ctypes.c_float), ("const_hi", ctypes.c_float),
+                ("p_const", ctypes.c_float), ("p_leaf", ctypes.c_float), ("p_modi", ctypes.c_float),
+                ("depth_min", ctypes.c_int32), ("depth_max", ctypes.c_int32),
+                ("tournament_size", ctypes.c_int32), ("p_crossover", ctypes.c_float),
+                ("p_mutation", ctypes.c_float), ("crossover_kind", ctypes.c_int32),
+                ("leaf_bias", ctypes.c_float), ("mutation_weights", ctypes.c_float * 8),
+                ("point_rate", ctypes.c_float), ("const_sigma", ctypes.c_float),
+                ("subtree_depth", ctypes.c_int32)]
+
+
+def make_cfg(d: dict) -> OvCfg:
+    """dict with the OvCfg field names (mutation_weights: 8 floats, funcs: ids)."""
+    c = OvCfg()
+    for k, v in d.items():
+        if k == "funcs":
+            c.func_mask = sum(1 << int(f) for f in v)
+        elif k == "mutation_weights":
+            c.mutation_weights = (ctypes.c_float * 8)(*v)
+        else:
+            setattr(c, k, v)
+    return c
+
+
+def draw(seed: int, stream: int, purpose: int, index: int) -> int:
+    """Reading R16 counter-based draw (uint32)."""
+    return int(_load().orv_draw(seed, stream, (purpose << 32) | index))
+
+
+def exchange(old_t, old_v, old_s, parent, k, don_t, don_v, don_s, donor, j, max_len: int):
+    """Batched subtree exchange (§III-B). Returns (t, v, s, rejected)."""
+    lib = _load()
+    old_t, old_v, old_s = (np.ascontiguousarray(a) for a in (old_t, old_v, old_s))
+    don_t, don_v, don_s = (np.ascontiguousarray(a) for a in (don_t, don_v, don_s))
+    parent, k, donor, j = (np.ascontiguousarray(a, dtype=np.int32) for a in (parent, k, donor, j))
+    n = len(parent)
+    ld = old_t.shape[1]
+    ot = np.zeros((n, max_len), np.int16)
+    ov = np.zeros((n, max_len), np.float32)
+    os_ = np.zeros((n, max_len), np.int16)
+    rej = np.zeros(n, np.uint8)
+    st = lib.oracle_exchange(n, _p(old_t), _p(old_v), _p(old_s), ld, _p(parent), _p(k), _p(don_t), _p(don_v),
+                             _p(don_s), _p(donor), _p(j), max_len, _p(ot), _p(ov), _p(os_), _p(rej))
+    if st != OK:
+        raise OracleError(st)
+    return ot, ov, os_, rej.astype(bool)
+
+
+def tournament(fit, T: int, n_winners: int, seed: int, purpose: int = 1):
+    """Tournament selection (Algorithm 1 "Select parents"; size P:477; R17)."""
+    fit = np.ascontiguousarray(fit, dtype=np.float64)
+    w = np.zeros(n_winners, np.int32)
+    st = _load().oracle_tournament(_p(fit), len(fit), T, n_winners, seed, purpose, _p(w))
+    if st != OK:
+        raise OracleError(st)
+    return w
+
+
+def generate(P: int, cfg: dict, seed: int):
+    """Ramped half-and-half initial population (Algorithm 1; R19)."""
+    c = make_cfg(cfg)
+    L = c.max_len
+    t = np.zeros((P, L), np.int16)
+    v = np.zeros((P, L), np.float32)
+    s = np.zeros((P, L), np.int16)
+    st = _load().oracle_generate(P, ctypes.byref(c), seed, _p(t), _p(v), _p(s))
+    if st != OK:
+        raise OracleError(st)
+    return t, v, s
+
+
+def reproduce(t, v, s, fit, n_children: int, cfg: dict, seed: int):
+    """Algorithm 1 loop body (R18): returns (t, v, s, parents[n,2], ops[n])."""
+    c = make_cfg(cfg)
+    L = c.max_len
+    t, v, s = (np.ascontiguousarray(a) for a in (t, v, s))
+    fit = np.ascontiguousarray(fit, dtype=np.float64)
+    P, ld = t.shape
+    ot = np.zeros((n_children, L), np.int16)
+    ov = np.zeros((n_children, L), np.float32)
+    os_ = np.zeros((n_children, L), np.int16)
+    par = np.zeros((n_children, 2), np.int32)
+    ops = np.zeros(n_children, np.int32)
+    st = _load().oracle_reproduce(_p(t), _p(v), _p(s), P, ld, _p(fit), n_children, ctypes.byref(c), seed,
+                                  _p(ot), _p(ov), _p(os_), _p(par), _p(ops))
+    if st != OK:
+        raise OracleError(st)
+    return ot, ov, os_, par, ops
