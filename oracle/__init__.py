@@ -67,7 +67,7 @@ def _load():
             lib.oracle_tournament.restype = ctypes.c_int
             lib.oracle_generate.argtypes = [i64, vp, u64, vp, vp, vp]
             lib.oracle_generate.restype = ctypes.c_int
-            lib.oracle_reproduce.argtypes = [vp, vp, vp, i64, i32, vp, i64, vp, u64, vp, vp, vp, vp, vp]
+            lib.oracle_reproduce.argtypes = [vp, vp, vp, i64, i32, vp, i64, i64, vp, u64, vp, vp, vp, vp, vp]
             lib.oracle_reproduce.restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -297,7 +297,7 @@ def generate(P: int, cfg: dict, seed: int):
     return t, v, s
 
 
-def reproduce(t, v, s, fit, n_children: int, cfg: dict, seed: int):
+def reproduce(t, v, s, fit, n_children: int, cfg: dict, seed: int, child0: int = 0):
     """Algorithm 1 loop body (R18): returns (t, v, s, parents[n,2], ops[n])."""
     c = make_cfg(cfg)
     L = c.max_len
@@ -309,7 +309,7 @@ def reproduce(t, v, s, fit, n_children: int, cfg: dict, seed: int):
     os_ = np.zeros((n_children, L), np.int16)
     par = np.zeros((n_children, 2), np.int32)
     ops = np.zeros(n_children, np.int32)
-    st = _load().oracle_reproduce(_p(t), _p(v), _p(s), P, ld, _p(fit), n_children, ctypes.byref(c), seed,
+    st = _load().oracle_reproduce(_p(t), _p(v), _p(s), P, ld, _p(fit), n_children, child0, ctypes.byref(c), seed,
                                   _p(ot), _p(ov), _p(os_), _p(par), _p(ops))
     if st != OK:
         raise OracleError(st)

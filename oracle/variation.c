@@ -413,7 +413,7 @@ static int ov_mut_kind(const OvCfg* c, uint32_t u) {
 #define OP_MUT_NOP 0x100
 
 int oracle_reproduce(const int16_t* pt, const float* pv, const int16_t* ps, int64_t P, int32_t ld,
-                     const double* fit, int64_t n_children, const OvCfg* c, uint64_t seed, int16_t* out_t,
+                     const double* fit, int64_t n_children, int64_t child0, const OvCfg* c, uint64_t seed, int16_t* out_t,
                      float* out_v, int16_t* out_s, int32_t* parents, int32_t* ops) {
   int L = c->max_len;
   if (P < 1 || ld < L || c->tournament_size < 1) return OV_E_ARG;
@@ -421,7 +421,7 @@ int oracle_reproduce(const int16_t* pt, const float* pv, const int16_t* ps, int6
   float *av = malloc(4 * L), *bv = malloc(4 * L), *gv = malloc(4 * L);
   int16_t *as = malloc(2 * L), *bs = malloc(2 * L), *gs = malloc(2 * L);
   for (int64_t ci = 0; ci < n_children; ci++) {
-    uint64_t st = (uint64_t)ci;
+    uint64_t st = (uint64_t)(child0 + ci); /* stream = global child index */
     int op = 0;
     /* Select parents */
     int64_t p1 = ov_tournament1(fit, P, c->tournament_size, seed, st, PUR_TOUR1);

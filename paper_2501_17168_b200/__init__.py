@@ -24,6 +24,7 @@ _LIB = _lib.load()
 __all__ = [
     "tensorize", "eval", "sr_fitness", "sr_sse", "classification_accuracy", "eval_paired", "select_strategy", "workspace_size", "Workspace",
     "check_device_flags", "EvogpError", "last_launch_count", "set_kernel_timing", "STRATEGIES",
+    "GPConfig", "generate", "subtree_exchange", "tournament", "reproduce", "Evolution",
 ]
 
 STRATEGIES = {"auto": STRATEGY_AUTO, "inter": STRATEGY_INTER, "intra": STRATEGY_INTRA,
@@ -266,3 +267,6 @@ def set_kernel_timing(start_event=None, end_event=None) -> None:
     st = _LIB.evogp_set_kernel_timing(a, b)
     if st != OK:
         raise EvogpError(st, "evogp_set_kernel_timing")
+
+
+from .gp import Evolution, GPConfig, generate, reproduce, subtree_exchange, tournament  # noqa: E402

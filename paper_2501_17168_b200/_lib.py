@@ -23,7 +23,7 @@ EXPORTS = (
     "evogp_tensorize", "evogp_workspace_size", "evogp_eval", "evogp_sr_fitness", "evogp_sr_sse",
     "evogp_select_strategy", "evogp_check_device_flags", "evogp_status_string", "evogp_last_error",
     "evogp_last_launch_count", "evogp_set_kernel_timing", "evogp_classification_accuracy",
-    "evogp_eval_paired",
+    "evogp_eval_paired", "evogp_generate", "evogp_subtree_exchange", "evogp_tournament", "evogp_reproduce",
 )
 
 
@@ -49,6 +49,16 @@ def load() -> ctypes.CDLL:
     lib.evogp_classification_accuracy.restype = ctypes.c_int
     lib.evogp_eval_paired.argtypes = [vp, vp, vp, i64, i32, i32, vp, i32, i32, i32, vp, vp, sz, vp]
     lib.evogp_eval_paired.restype = ctypes.c_int
+    u64 = ctypes.c_uint64
+    lib.evogp_generate.argtypes = [i64, vp, u64, vp, vp, vp, vp]
+    lib.evogp_generate.restype = ctypes.c_int
+    lib.evogp_subtree_exchange.argtypes = [i64, vp, vp, vp, i32, vp, vp, vp, vp, vp, i32, vp, vp, i32, vp, vp, vp,
+                                           vp, vp]
+    lib.evogp_subtree_exchange.restype = ctypes.c_int
+    lib.evogp_tournament.argtypes = [vp, i64, i32, i64, u64, i32, vp, vp]
+    lib.evogp_tournament.restype = ctypes.c_int
+    lib.evogp_reproduce.argtypes = [vp, vp, vp, i64, i32, vp, i64, i64, vp, u64, vp, vp, vp, vp, vp, vp]
+    lib.evogp_reproduce.restype = ctypes.c_int
     lib.evogp_select_strategy.argtypes = [i64, i64, i32, i32, i32]
     lib.evogp_select_strategy.restype = ctypes.c_int
     lib.evogp_check_device_flags.argtypes = [vp, vp, vp]

@@ -1,0 +1,247 @@
+"""GPU parity for the genetic operators,
+through the C-ABI, against oracle/variation.c on the same seeded inputs.
+Integer / structural work, so the bar is bit-exact: type, size and the
+value bits of every row, the parents chosen and the op record of every
+child. Random decisions are the counter-based draws of DESIGN.md R16, which
+both sides implement independently.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _e():
+    import paper_2501_17168_b200 as evogp
+
+    return evogp
+
+
+def cfg_dict(**kw):
+    c = dict(max_len=63, n_inputs=4, n_outputs=1, funcs=[0, 1, 2, 3, 4, 5, 6], const_lo=-1.0, const_hi=1.0,
+             p_const=0.5, p_leaf=0.1, p_modi=0.0, depth_min=2, depth_max=6, tournament_size=20, p_crossover=0.9,
+             p_mutation=0.1, crossover_kind=0, leaf_bias=0.1, mutation_weights=[1.0] + [0.0] * 7, point_rate=0.1,
+             const_sigma=0.1, subtree_depth=4)
+    c.update(kw)
+    return c
+
+
+def gp_cfg(d):
+    e = _e()
+    d = dict(d)
+    d["funcs"] = tuple(d["funcs"])
+    d["mutation_weights"] = tuple(d["mutation_weights"])
+    return e.GPConfig(**d)
+
+
+def dev_rows(t, v, s):
+    return tuple(torch.from_numpy(np.ascontiguousarray(a)).to(DEV) for a in (t, v, s))
+
+
+def host(rows):
+    return tuple(a.cpu().numpy() for a in rows)
+
+
+def assert_rows_equal(g, r, what=""):
+    gt, gv, gs = g
+    rt, rv, rs = r
+    bad = np.nonzero(~((gt == rt).all(1) & (gs == rs).all(1) & (gv.view(np.uint32) == rv.view(np.uint32)).all(1)))[0]
+    assert bad.size == 0, f"{what}: {bad.size} rows differ, first {bad[:5]}"
+
+
+def synth_pop(P, L, n_in=4, n_out=1, seed=11, mix=synth.M_FULL, modi=0.0):
+    pt = synth.trees(seed, 0, P, L, mix, n_in, n_out, modi)
+    return oracle.tensorize(pt.offsets, pt.types, pt.values, L, n_in, n_out)
+
+
+# ------------------------------------------------------------------ generate
+@pytest.mark.parametrize("L,n_out,dmin,dmax,funcs", [
+    (15, 1, 1, 8, list(range(22))),
+    (63, 1, 2, 6, [0, 1, 2, 3, 4, 5, 6]),
+    (63, 6, 2, 6, list(range(22))),
+    (512, 1, 2, 10, [0, 1, 2, 3, 4, 5, 6]),
+    (2048, 1, 3, 12, [0, 21, 4]),
+])
+def test_generate_bitexact(L, n_out, dmin, dmax, funcs):
+    e = _e()
+    d = cfg_dict(max_len=L, n_outputs=n_out, depth_min=dmin, depth_max=dmax, funcs=funcs, p_modi=0.2)
+    P = 3000 if L <= 512 else 300
+    g = host(e.generate(P, gp_cfg(d), 4242, device=DEV))
+    r = oracle.generate(P, d, 4242)
+    assert_rows_equal(g, r, f"generate L={L}")
+
+
+def test_generate_empty():
+    e = _e()
+    t, v, s = e.generate(0, gp_cfg(cfg_dict()), 1, device=DEV)
+    assert t.shape == (0, 63)
+
+
+# ------------------------------------------------------------------ exchange
+@pytest.mark.parametrize("L", [31, 127])
+def test_exchange_bitexact(L):
+    e = _e()
+    P = 500
+    t, v, s = synth_pop(P, L, seed=3)
+    rng = np.random.default_rng(7)
+    n = 20000
+    par = rng.integers(0, P, n).astype(np.int32)
+    don = rng.integers(0, P, n).astype(np.int32)
+    ks = np.array([rng.integers(0, s[p, 0]) for p in par], np.int32)
+    js = np.array([rng.integers(0, s[d, 0]) for d in don], np.int32)
+    rt, rv, rs, rej = oracle.exchange(t, v, s, par, ks, t, v, s, don, js, L)
+    pop = dev_rows(t, v, s)
+    idx = [torch.from_numpy(a).to(DEV) for a in (par, ks, don, js)]
+    gt, gv, gs, grej = e.subtree_exchange(pop, idx[0], idx[1], pop, idx[2], idx[3], L)
+    assert_rows_equal(host((gt, gv, gs)), (rt, rv, rs), "exchange")
+    assert (grej.cpu().numpy() == rej.astype(np.uint8)).all()
+    assert 0 < rej.sum() < n
+
+
+def test_exchange_bad_index_and_ld():
+    """Out-of-range k / j reject with code 2 and copy T_old; donors may use another stride."""
+    e = _e()
+    L = 31
+    t, v, s = synth_pop(50, L, seed=4)
+    ld = 40
+    dt = np.full((50, ld), -1, np.int16)
+    dv = np.full((50, ld), np.nan, np.float32)
+    ds = np.zeros((50, ld), np.int16)
+    dt[:, :L], dv[:, :L], ds[:, :L] = t, v, s
+    par = np.arange(50, dtype=np.int32)
+    k = np.zeros(50, np.int32)
+    k[:5] = s[:5, 0]  # one past the end
+    j = np.zeros(50, np.int32)
+    j[5:10] = -1
+    don = par[::-1].copy()
+    idx = [torch.from_numpy(a).to(DEV) for a in (par, k, don, j)]
+    gt, gv, gs, grej = e.subtree_exchange(dev_rows(t, v, s), idx[0], idx[1], dev_rows(dt, dv, ds), idx[2], idx[3], L)
+    grej = grej.cpu().numpy()
+    assert (grej[:10] == 2).all()
+    g = host((gt, gv, gs))
+    assert_rows_equal(tuple(a[:10] for a in g), (t[:10], v[:10], s[:10]), "bad index copies")
+    rt, rv, rs, rej = oracle.exchange(t, v, s, par[10:], k[10:], t, v, s, don[10:], j[10:], L)
+    assert_rows_equal(tuple(a[10:] for a in g), (rt, rv, rs), "stride-40 donors")
+
+
+# ---------------------------------------------------------------- tournament
+@pytest.mark.parametrize("P,T", [(1, 1), (50, 1), (1000, 20), (1000, 100), (10 ** 6, 20)])
+def test_tournament_bitexact(P, T):
+    e = _e()
+    rng = np.random.default_rng(P + T)
+    fit = rng.integers(0, 50, P).astype(np.float64)  # many ties
+    fit[rng.integers(0, P, max(1, P // 10))] = np.nan
+    fit[rng.integers(0, P, max(1, P // 20))] = np.inf
+    n = min(P, 100000) if P > 1 else 10
+    for pur in (1, 2):
+        g = e.tournament(torch.from_numpy(fit).to(DEV), T, n, 777, purpose=pur).cpu().numpy()
+        r = oracle.tournament(fit, T, n, 777, purpose=pur)
+        assert (g == r).all()
+
+
+# ---------------------------------------------------------------- reproduce
+MUTS = ["subtree", "hoist", "point", "multi_point", "insert", "delete", "const", "multi_const"]
+CASES = [("one_point", dict(crossover_kind=0, p_mutation=0.0)),
+         ("leaf_biased", dict(crossover_kind=1, leaf_bias=0.3, p_mutation=0.0))] + \
+        [(m, dict(p_crossover=0.5, p_mutation=1.0, mutation_weights=[float(q == i) for q in range(8)]))
+         for i, m in enumerate(MUTS)] + \
+        [("mixed", dict(p_mutation=0.5, mutation_weights=[1, 2, 1, 1, 3, 1, 1, 2]))]
+
+
+@pytest.mark.parametrize("name,kw", CASES, ids=[c[0] for c in CASES])
+@pytest.mark.parametrize("L", [31, 255])
+def test_reproduce_bitexact(name, kw, L):
+    e = _e()
+    d = cfg_dict(max_len=L, funcs=list(range(22)), point_rate=0.3, **kw)
+    P = 2000
+    t, v, s = synth_pop(P, L, seed=21)
+    fit = np.random.default_rng(3).random(P)
+    fit[::7] = np.nan
+    n, child0, seed = 5000, 123, 98765
+    rt, rv, rs, rpar, rops = oracle.reproduce(t, v, s, fit, n, d, seed, child0=child0)
+    gt, gv, gs, gpar, gops = e.reproduce(dev_rows(t, v, s), torch.from_numpy(fit).to(DEV), n, gp_cfg(d), seed,
+                                         child0=child0)
+    assert (gpar.cpu().numpy() == rpar).all()
+    assert (gops.cpu().numpy() == rops).all()
+    assert_rows_equal(host((gt, gv, gs)), (rt, rv, rs), f"reproduce {name}")
+
+
+def test_reproduce_multi_output_and_stride():
+    """Modi populations (6 outputs) with parent rows of stride ld > max_len."""
+    e = _e()
+    L, ld, P = 63, 64, 1000
+    d = cfg_dict(max_len=L, n_outputs=6, p_modi=0.2, funcs=list(range(22)), p_mutation=0.7,
+                 mutation_weights=[1] * 8)
+    t, v, s = oracle.generate(P, d, 5)
+    tt = np.full((P, ld), -1, np.int16)
+    vv = np.full((P, ld), np.nan, np.float32)
+    ss = np.zeros((P, ld), np.int16)
+    tt[:, :L], vv[:, :L], ss[:, :L] = t, v, s
+    fit = np.random.default_rng(1).random(P)
+    rt, rv, rs, rpar, rops = oracle.reproduce(t, v, s, fit, 3000, d, 55)
+    gt, gv, gs, gpar, gops = e.reproduce(dev_rows(tt, vv, ss), torch.from_numpy(fit).to(DEV), 3000, gp_cfg(d), 55)
+    assert (gops.cpu().numpy() == rops).all()
+    assert_rows_equal(host((gt, gv, gs)), (rt, rv, rs), "multi-output")
+
+
+def test_reproduce_full_size_loop_config():
+    """The loop bench's shape (P = 10^5, max_len 512, tab:sr_params), every child."""
+    e = _e()
+    L, P = 512, 100000
+    d = cfg_dict(max_len=L, n_inputs=7, depth_min=2, depth_max=8, mutation_weights=[1, 1, 1, 1, 1, 1, 1, 1])
+    t, v, s = oracle.generate(P, d, 1)
+    g0 = host(e.generate(P, gp_cfg(d), 1, device=DEV))
+    assert_rows_equal(g0, (t, v, s), "generate 1e5 x 512")
+    fit = np.random.default_rng(2).random(P)
+    rt, rv, rs, rpar, rops = oracle.reproduce(t, v, s, fit, P, d, 3)
+    gt, gv, gs, gpar, gops = e.reproduce(dev_rows(t, v, s), torch.from_numpy(fit).to(DEV), P, gp_cfg(d), 3)
+    assert (gops.cpu().numpy() == rops).all()
+    assert_rows_equal(host((gt, gv, gs)), (rt, rv, rs), "reproduce 1e5 x 512")
+
+
+def test_generational_loop_matches_oracle_loop():
+    """Algorithm 1 for a few generations: GPU reproduce fed the ORACLE's fitness
+    of the current population equals the oracle's own loop at every generation
+    (IEEE mix, so the populations evaluated are identical)."""
+    e = _e()
+    L, P, D = 63, 500, 64
+    d = cfg_dict(max_len=L, n_inputs=2, funcs=list(synth.M_IEEE), p_mutation=0.3, mutation_weights=[1] * 8)
+    X = synth.dataset_X(9, 0, D, 2)
+    y = synth.pagie_y(X)
+    ot, ov, os_ = oracle.generate(P, d, 10)
+    gpop = e.generate(P, gp_cfg(d), 10, device=DEV)
+    for gen in range(5):
+        assert_rows_equal(host(gpop), (ot, ov, os_), f"generation {gen}")
+        fit = oracle.mse(oracle.evaluate(ot, ov, os_, X, mode=1)[:, :, 0], y)
+        ot, ov, os_, _, _ = oracle.reproduce(ot, ov, os_, fit, P, d, 100 + gen)
+        gt, gv, gs, _, _ = e.reproduce(gpop, torch.from_numpy(fit).to(DEV), P, gp_cfg(d), 100 + gen)
+        gpop = (gt, gv, gs)
+
+
+def test_evolution_runs_and_improves():
+    """Evolution (Algorithm 1, device-resident): rows stay valid; the best MSE
+    after 15 generations beats the initial best on the Pagie target."""
+    e = _e()
+    L, P, D = 63, 4096, 256
+    cfg = e.GPConfig(max_len=L, n_inputs=2, mutation_weights=(1, 1, 1, 1, 1, 1, 1, 1), p_mutation=0.2)
+    X = synth.dataset_X(9, 0, D, 2, "uniform", -5.0, 5.0)
+    y = synth.pagie_y(X)
+    ev = e.Evolution(P, cfg, torch.from_numpy(X).to(DEV), torch.from_numpy(y).to(DEV), seed=3)
+    best0 = np.nanmin(ev.evaluate().cpu().numpy())
+    for _ in range(15):
+        ev.step()
+    fit = ev.evaluate().cpu().numpy()
+    assert np.nanmin(fit) < best0
+    t, v, s = host(ev.population)
+    lens = s[:, 0].astype(np.int64)
+    off = np.concatenate([[0], np.cumsum(lens)])
+    types = np.concatenate([t[i, :lens[i]] for i in range(P)])
+    vals = np.concatenate([v[i, :lens[i]] for i in range(P)])
+    _, _, rs = oracle.tensorize(off, types, vals, L, 2, 1)
+    assert (rs == s).all()
