@@ -230,11 +230,249 @@ def run_reference(args, cfg, mix):
     return 0
 
 
+
+# ---------------------------------------------------------------- NEXT-4: the whole generational loop
+def loop_gp_config(cfg):
+    """tab:sr_params: max size 512, tournament 20, p_c 0.9, p_m 0.1,
+    {+,-,x,/,sin,cos,tan}; subtree mutation (Algorithm 1's classic loop, R18)."""
+    from paper_2501_17168_b200.gp import GPConfig
+
+    return GPConfig(max_len=cfg.max_len, n_inputs=cfg.n_in, n_outputs=1, funcs=tuple(synth.M_PAPER),
+                    tournament_size=20, p_crossover=0.9, p_mutation=0.1, depth_min=2, depth_max=6,
+                    subtree_depth=4, mutation_weights=(1, 0, 0, 0, 0, 0, 0, 0))
+
+
+def loop_oracle_sample(cfg, seconds, warm_gens=0):
+    """The oracle's Algorithm 1 on a bounded sample: a 2,000-tree population of
+    the same configuration, generations of (evaluate + MSE + reproduce) for
+    about `seconds`. Returns (GPops/s, description)."""
+    import oracle
+
+    gp = loop_gp_config(cfg)
+    d = {k: getattr(gp, k) for k in ("max_len", "n_inputs", "n_outputs", "const_lo", "const_hi", "p_const",
+                                     "p_leaf", "p_modi", "depth_min", "depth_max", "tournament_size",
+                                     "p_crossover", "p_mutation", "crossover_kind", "leaf_bias", "point_rate",
+                                     "const_sigma", "subtree_depth")}
+    d["funcs"] = list(gp.funcs)
+    d["mutation_weights"] = list(gp.mutation_weights)
+    n = 2000
+    X, y = synth.config_data(cfg)
+    t, v, s = oracle.generate(n, d, cfg.seed)
+    threads = os.cpu_count() or 1
+    work, gens = 0.0, 0
+    t0 = time.perf_counter()
+    while True:
+        work += float(s[:, 0].astype(np.int64).sum()) * cfg.D
+        fit = oracle.mse(oracle.evaluate(t, v, s, X, mode=0, threads=threads)[:, :, 0], y)
+        t, v, s, _, _ = oracle.reproduce(t, v, s, fit, n, d, cfg.seed + 1 + gens)
+        gens += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or gens >= 100:
+            break
+    desc = (f"Algorithm 1 on a {n}-tree population of {cfg.name} (D={cfg.D}), {gens} generations from the "
+            f"initial population in {el:.1f} s")
+    return work / el, desc, threads
+
+
+def run_loop(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_17168_b200 as evogp
+
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        value, desc, threads = loop_oracle_sample(cfg, args.cpu_seconds)
+        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"{cfg.name}: Algorithm 1, P={cfg.P}, max_len={cfg.max_len}, "
+                                       f"n_inputs={cfg.n_in}, D={cfg.D}", "parallelism": "host threads (oracle)"},
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    gp = loop_gp_config(cfg)
+    X, y = synth.config_data(cfg)
+    Xd, yd = torch.from_numpy(X).to(dev), torch.from_numpy(y).to(dev)
+    P = cfg.P
+    # island model across ranks (DESIGN.md §10): rank r evolves its own P trees
+    seed = cfg.seed + 1_000_003 * rank
+    strategy = evogp.select_strategy(P, cfg.D, cfg.max_len, 1, local)
+    ws = evogp.Workspace(P, cfg.D, cfg.max_len, cfg.n_in, 1, device=dev)
+
+    launches = [0]
+
+    def make_run():
+        ev = evogp.Evolution(P, gp, Xd, yd, seed=seed, strategy=strategy)
+        ev.ws = ws
+        return ev
+
+    def gen_step(ev, kev=None, rev=None):
+        """One generation of Algorithm 1: fused SR fitness, then reproduction."""
+        t, v, s = ev.population
+        if kev is not None:
+            evogp.set_kernel_timing(*kev)
+        evogp.sr_fitness(t, v, s, Xd, yd, strategy=strategy, out=ev.fitness, workspace=ws)
+        launches[0] += evogp.last_launch_count() + 1  # + the reproduce kernel
+        if kev is not None:
+            evogp.set_kernel_timing(None, None)
+        if rev is not None:
+            rev[0].record()
+        nxt = 1 - ev.cur
+        evogp.reproduce(ev.population, ev.fitness, P, gp, ev.seed + 1 + ev.generation, out=ev.bufs[nxt],
+                        record=False)
+        if rev is not None:
+            rev[1].record()
+        ev.cur = nxt
+        ev.generation += 1
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sampler = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local])
+                           if "CUDA_VISIBLE_DEVICES" in os.environ else local)
+    sampler.start()
+    # sustain the load for the clock sampler (untimed, a throwaway run)
+    warm = make_run()
+    t_end = time.perf_counter() + args.sustain_seconds
+    while True:
+        gen_step(warm)
+        torch.cuda.synchronize()
+        if time.perf_counter() >= t_end:
+            break
+    del warm
+    run = make_run()
+    for _ in range(args.warmup):
+        gen_step(run)
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    rev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for a, b in kev:
+        a.record()
+        b.record()
+    lens = torch.zeros(K, dtype=torch.int64, device=dev)
+    barrier()
+    launches[0] = 0
+    for i in range(K):
+        ev[i][0].record()
+        gen_step(run, kev[i], rev[i])
+        ev[i][1].record()
+        # bookkeeping outside the events: nodes of the population just evaluated
+        t_prev, v_prev, s_prev = run.bufs[1 - run.cur]
+        lens[i] = s_prev[:, 0].to(torch.int64).sum()
+    barrier()
+    timed_launches = launches[0]
+    clocks = sampler.stop()
+    step_ms = sum(a.elapsed_time(b) for a, b in ev)
+    kern_ms = sum(a.elapsed_time(b) for a, b in kev)
+    rep_ms = sum(a.elapsed_time(b) for a, b in rev)
+    nodes_per_gen = lens.to(torch.float64)
+    work_local = float(nodes_per_gen.sum().item()) * cfg.D
+    tt = torch.tensor([step_ms, kern_ms, rep_ms], dtype=torch.float64, device=dev)
+    work = torch.tensor([work_local], dtype=torch.float64, device=dev)
+    best = torch.nan_to_num(run.evaluate(), nan=float("inf")).min().reshape(1)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(work, op=dist.ReduceOp.SUM)
+        dist.all_reduce(best, op=dist.ReduceOp.MIN)
+    step_ms, kern_ms, rep_ms = tt.tolist()
+    value = work.item() / (step_ms * 1e-3)
+    mean_len = float(nodes_per_gen.mean().item()) / P
+
+    # ---- e2e: Algorithm 1 through the public API from host data: X, y copied
+    # from pinned host memory, the population generated on the device, and the
+    # best fitness read back every generation (Algorithm 1's target check)
+    e2e = None
+    if not args.no_e2e:
+        h_X, h_y = torch.from_numpy(X).pin_memory(), torch.from_numpy(y).pin_memory()
+        h_best = torch.empty(1, dtype=torch.float64).pin_memory()
+        barrier()
+        t0 = time.perf_counter()
+        Xd.copy_(h_X, non_blocking=True)
+        yd.copy_(h_y, non_blocking=True)
+        r2 = make_run()
+        for _ in range(args.warmup + K):
+            gen_step(r2)
+            h_best.copy_(torch.nan_to_num(r2.fitness, nan=float("inf")).min().reshape(1), non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        barrier()
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        # same seeds -> the same populations as the timed run: its node counts apply
+        # (warm-up generations counted at the first timed generation's size, a lower bound)
+        e2e_nodes = float(nodes_per_gen.sum().item()) + args.warmup * float(nodes_per_gen[0].item())
+        e2e = {"value": e2e_nodes * cfg.D * world / el.item(), "unit": UNIT,
+               "h2d_bytes_per_step": int((X.nbytes + y.nbytes) / (args.warmup + K)),
+               "d2h_bytes_per_step": 8,
+               "includes": "H2D of X, y + on-device generation + (fitness + reproduce + best-fitness D2H) "
+                           f"x {args.warmup + K} generations, wall clock"}
+
+    if rank == 0:
+        peaks, peak_src = measured_peaks()
+        f = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        # SFU-node fraction (/, sin, cos, tan of the paper set), measured on the
+        # last population evaluated
+        t, v, s = run.bufs[1 - run.cur]
+        tl = t.to(torch.int32) & 7
+        fn = tl >= 2
+        vals = v[fn].to(torch.int64)
+        n_sfu = torch.isin(vals, torch.tensor(SFU_FUNCS, device=dev)).sum().item()
+        n_nodes = (s[:, 0].to(torch.int64)).sum().item()
+        sfu_frac = n_sfu / max(1, n_nodes)
+        roof = 1.0 / max(1.0 / (SMS * FP32_LANES * f), sfu_frac / (SMS * SFU_LANES * f))
+        achieved = work_local / (kern_ms * 1e-3)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": step_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: Algorithm 1 (fitness + tournament + crossover + mutation per "
+                                   f"generation), P={P} per rank, max_len={cfg.max_len}, n_inputs={cfg.n_in}, "
+                                   f"D={cfg.D}, mix=paper, tab:sr_params",
+                       "P_per_rank": P, "D": cfg.D, "max_len": cfg.max_len, "mean_len": mean_len,
+                       "generations_timed": K, "generation_of_first_timed": args.warmup,
+                       "strategy": strategy, "parallelism": f"islands x{world}",
+                       "best_mse_final": float(best.item()),
+                       "l2": "inputs larger than L2 (population rows 2 x P x max_len x 8 B)",
+                       "step": "one generation: evogp_sr_fitness + evogp_reproduce",
+                       "paper_context": "1.00e11 GPops/s, RTX 4090, P=1e5, D=392, S=482 (P:592)"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": roof, "unit": UNIT, "frac": achieved / roof,
+                         "traffic": None, "kernel": f"k_{strategy} (fitness)",
+                         "peak_basis": f"{SMS} SMs x min({FP32_LANES} FP32, {SFU_LANES}/s MUFU) lanes/clk at "
+                                       f"sm_max_mhz={f / 1e6:.0f} ({peak_src}), s={sfu_frac:.3f}",
+                         "step_share": {"fitness": kern_ms / step_ms, "reproduce": rep_ms / step_ms}},
+            "gpu_launches": timed_launches,
+            "clocks": clocks,
+            "e2e": e2e,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            cv, desc, threads = loop_oracle_sample(cfg, args.cpu_seconds)
+            line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     args = parse()
     cfg = synth.CONFIGS[args.config]
     mix = args.mix or default_mix(cfg)
+    if cfg.loop:
+        return run_loop(args, cfg)
     if args.impl == "reference":
         return run_reference(args, cfg, mix)
 

@@ -79,6 +79,7 @@ int run(int mode, const int16_t* type, const float* value, const int16_t* size, 
   kp.partials = reinterpret_cast<double*>(ws + pl.off_partials);
   kp.deep_locks = reinterpret_cast<int32_t*>(ws + pl.off_locks);
   kp.deep = reinterpret_cast<float*>(ws + pl.off_deep);
+  kp.deep_pw = reinterpret_cast<float*>(ws + pl.off_deep_pw);
   kp.prog = reinterpret_cast<Node*>(ws + pl.off_prog);
   kp.info = reinterpret_cast<TreeMeta*>(ws + pl.off_info);
   int nl = 0;

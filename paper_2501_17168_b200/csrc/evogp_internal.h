@@ -117,6 +117,10 @@ struct KParams {
   Control* ctl;
   int32_t* deep_locks;
   float* deep;
+  // per-warp private global stacks (no locks): grid x warps slots of
+  // deep_pw_levels K-point levels; rows needing more use the locked pool
+  float* deep_pw;
+  int32_t deep_pw_levels;
 };
 
 struct Plan {
@@ -127,7 +131,7 @@ struct Plan {
   size_t smem_bytes;
   KParams kp;
   // workspace layout
-  size_t off_ctl, off_xs, off_counters, off_partials, off_locks, off_deep, off_prog, off_info, total;
+  size_t off_ctl, off_xs, off_counters, off_partials, off_locks, off_deep, off_deep_pw, off_prog, off_info, total;
 };
 
 // kernels.cu

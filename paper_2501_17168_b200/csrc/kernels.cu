@@ -499,13 +499,45 @@ __device__ __forceinline__ void zero_acc(float* s_acc_l, int n_out) {
 // Evaluate `tree` on one chunk: the hot copy (shared-memory stack, no calls)
 // unless the row is deeper than the shared slots; a chunk in which any lane
 // left a fast path's range is re-run on the cold copy.
+// NP passes of H = K/NP points each over the warp's shared slots: the SD
+// K-point slots hold NP*SD H-point slots. The H-point layout of pass q is the
+// slice of the K layout [K/4 groups][32 lanes][4] starting at point H*q of
+// every lane (H divides 4), so pass q yields tos[H*q .. H*q+H-1] — the same
+// values, in the same order of operations, as a single K-point run.
+template <int K, int H>
+__device__ __forceinline__ void run_passes(const Node* tree, int len, const float* xl, int lane, float* s_stack_l,
+                                           float* s_acc_l, float (&tos)[K], unsigned* cold) {
+  constexpr int NP = K / H;
+  static_assert(H >= 1 && K % H == 0 && (H >= 4 || 4 % H == 0), "pass width");
+  float* stk = s_stack_l - lane * Lay<K>::V + lane * Lay<H>::V;
+#pragma unroll 1
+  for (int q = 0; q < NP; ++q) {
+    const float* xq = xl + (H * q / 4) * 128 + (H * q) % 4;
+    float th[H];
+    const bool bail = interpret<H, false, false>(tree, len, xq, stk, s_acc_l, th);
+    if (__any_sync(FULL_MASK, bail)) {
+      if (lane == 0) atomicAdd(cold, 1u);
+      interpret<H, false, true>(tree, len, xq, stk, s_acc_l, th);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (k / H == q) tos[k] = th[k % H];
+  }
+}
+
+// Evaluate `tree` on one chunk: the hot copy (shared-memory stack, no calls)
+// in as few passes as the row's depth allows; a chunk in which any lane left
+// a fast path's range is re-run on the cold copy. Rows deeper than every
+// pass split use a global stack: the warp's private slot (no contention) when
+// it is deep enough, else a slot of the locked pool.
 template <int K, bool MULTI>
 __device__ __forceinline__ void run_chunk(const KParams& p, const Node* tree, const TreeInfo& ti, int64_t chunk_base,
                                           int lane, float* s_stack_l, float* s_acc_l, float (&tos)[K]) {
   constexpr int V = Lay<K>::V;
   const float* xl = p.xs + chunk_base + lane * V;
   if (MULTI) zero_acc<K>(s_acc_l, p.n_out);
-  if (ti.maxdepth - 1 <= p.SD) {
+  const int need = ti.maxdepth - 1;  // stack slots below the register top
+  if (need <= p.SD) {
     const bool bail = interpret<K, MULTI, false>(tree, ti.len, xl, s_stack_l, s_acc_l, tos);
     if (__any_sync(FULL_MASK, bail)) {
       if (lane == 0) atomicAdd(&p.ctl->cold_chunks, 1u);
@@ -515,29 +547,36 @@ __device__ __forceinline__ void run_chunk(const KParams& p, const Node* tree, co
       }
       interpret<K, MULTI, true>(tree, ti.len, xl, s_stack_l, s_acc_l, tos);
     }
-  } else if (K >= 8 && !MULTI && ti.maxdepth - 1 <= 2 * p.SD) {
-    // Too deep for K-point slots: two K/2 passes over the same shared region
-    // hold twice the slots. The K/2 point layout is exactly half h of the K
-    // layout (groups 2h.. of [groups][32 lanes][4]), so pass h yields
-    // tos[K/2*h .. K/2*h + K/2 - 1] — the same values as a K-point run.
-    constexpr int H = K >= 8 ? K / 2 : 4;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float th[H];
-      const bool bail = interpret<H, false, false>(tree, ti.len, xl + h * 32 * H, s_stack_l, s_acc_l, th);
-      if (__any_sync(FULL_MASK, bail)) {
-        if (lane == 0) atomicAdd(&p.ctl->cold_chunks, 1u);
-        interpret<H, false, true>(tree, ti.len, xl + h * 32 * H, s_stack_l, s_acc_l, th);
-      }
-#pragma unroll
-      for (int k = 0; k < H; ++k) tos[(H * h + k) % K] = th[k];
-    }
-  } else {
-    const int slot = deep_acquire(p, lane);
-    interpret<K, MULTI, true>(tree, ti.len, xl, p.deep + static_cast<int64_t>(slot) * p.deep_slot_floats + lane * V,
-                              s_acc_l, tos);
-    deep_release(p, slot, lane);
+    return;
   }
+  if constexpr (!MULTI && K >= 2) {
+    if (need <= 2 * p.SD) {
+      run_passes<K, K / 2>(tree, ti.len, xl, lane, s_stack_l, s_acc_l, tos, &p.ctl->cold_chunks);
+      return;
+    }
+    if constexpr (K >= 4) {
+      if (need <= 4 * p.SD) {
+        run_passes<K, K / 4>(tree, ti.len, xl, lane, s_stack_l, s_acc_l, tos, &p.ctl->cold_chunks);
+        return;
+      }
+    }
+    if constexpr (K >= 8) {
+      if (need <= 8 * p.SD) {
+        run_passes<K, K / 8>(tree, ti.len, xl, lane, s_stack_l, s_acc_l, tos, &p.ctl->cold_chunks);
+        return;
+      }
+    }
+  }
+  if (need <= p.deep_pw_levels) {
+    const int64_t gw = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    interpret<K, MULTI, true>(tree, ti.len, xl, p.deep_pw + gw * p.deep_pw_levels * (32 * K) + lane * V, s_acc_l,
+                              tos);
+    return;
+  }
+  const int slot = deep_acquire(p, lane);
+  interpret<K, MULTI, true>(tree, ti.len, xl, p.deep + static_cast<int64_t>(slot) * p.deep_slot_floats + lane * V,
+                            s_acc_l, tos);
+  deep_release(p, slot, lane);
 }
 
 // ------------------------------------------------------------------------
@@ -766,6 +805,106 @@ __device__ int reorder_program(const Node* s_nodes, int n, Node* row, unsigned c
   return depth;
 }
 
+// Reordering + leaf fusion in one pass for deep single-output rows (lane 0):
+//  1. reverse scan with a stack of packed (size << 16 | need) entries, the
+//     top entry in a register: subtree sizes, Sethi-Ullman needs and the
+//     swap decision of every binary node (same rule as reorder_program);
+//  2. depth-first emission in the new prefix order (swapped binary nodes
+//     visit their second child first and take the reversed opcode), fusing a
+//     leaf that is the first-visited child of a unary / binary node (same
+//     rule as fuse_copy, applied to the reordered order), straight into the
+//     program row. Returns the new length; *depth = the row's stack need.
+// Scratch: 4 (L + 1) + 3 L bytes after the decoded nodes.
+__device__ int reorder_fuse_program(const Node* s_nodes, int n, Node* row, unsigned char* scr, int L, bool fuse,
+                                    int* depth) {
+  uint32_t* stk = reinterpret_cast<uint32_t*>(scr);       // L + 1 entries
+  uint16_t* sz = reinterpret_cast<uint16_t*>(stk + L + 1);  // subtree sizes
+  uint8_t* sw = reinterpret_cast<uint8_t*>(sz + L);         // swapped
+  int sp = 0;
+  uint32_t topv = 0;
+  for (int i = n - 1; i >= 0; --i) {
+    const uint32_t op = s_nodes[i + 1].w0 & 0xFFu;
+    const int ar = op <= OP_VAR ? 0 : func_arity(static_cast<int>(op) - OP_FN);
+    uint32_t r;
+    uint8_t swp = 0;
+    if (ar == 0) {
+      stk[sp++] = topv;
+      r = (1u << 16) | 1u;
+    } else if (ar == 1) {
+      r = topv + (1u << 16);
+    } else if (ar == 2) {
+      const uint32_t a = topv, b = stk[--sp];  // a = leftmost child (first pop)
+      const int qa = a & 0xFFFF, qb = b & 0xFFFF;
+      const int q_def = max(qb, qa + 1), q_swp = max(qa, qb + 1);
+      swp = q_swp < q_def;
+      r = ((1u + (a >> 16) + (b >> 16)) << 16) | static_cast<uint32_t>(swp ? q_swp : q_def);
+    } else {
+      const uint32_t a = topv, b = stk[--sp], c = stk[--sp];
+      const int q = max(static_cast<int>(c & 0xFFFF), max(static_cast<int>(b & 0xFFFF) + 1,
+                                                           static_cast<int>(a & 0xFFFF) + 2));
+      r = ((1u + (a >> 16) + (b >> 16) + (c >> 16)) << 16) | static_cast<uint32_t>(q);
+    }
+    topv = r;
+    sz[i] = static_cast<uint16_t>(r >> 16);
+    sw[i] = swp;
+  }
+  *depth = static_cast<int>(topv & 0xFFFF);
+  uint16_t* dstk = reinterpret_cast<uint16_t*>(stk);  // the scan stack is dead now
+  int out = 1, dsp = 0, i = 0;
+  row[0] = s_nodes[0];
+  for (;;) {
+    Node x = s_nodes[i + 1];
+    const uint32_t op = x.w0 & 0xFFu;
+    if (op <= OP_VAR) {
+      row[out++] = x;
+      if (dsp == 0) break;
+      i = dstk[--dsp];
+      continue;
+    }
+    const int ar = func_arity(static_cast<int>(op) - OP_FN);
+    const int c1 = i + 1;
+    if (ar == 1) {
+      const Node l = s_nodes[c1 + 1];
+      const uint32_t lop = l.w0 & 0xFFu;
+      if (fuse && lop <= OP_VAR && dsp > 0) {  // never absorb the last node
+        x.w0 = (x.w0 & ~0xFFu) | op | kFuse | (lop == OP_VAR ? kFuseVar : 0u);
+        x.w1 = l.w1;
+        row[out++] = x;
+        i = dstk[--dsp];
+      } else {
+        row[out++] = x;
+        i = c1;
+      }
+      continue;
+    }
+    const int c2 = c1 + sz[c1];
+    if (ar == 2) {
+      const bool swp = sw[i] != 0;
+      const uint32_t g = swp ? reversed_op(op) : op;
+      const int f1 = swp ? c2 : c1, f2 = swp ? c1 : c2;
+      const Node l = s_nodes[f1 + 1];
+      const uint32_t lop = l.w0 & 0xFFu;
+      if (fuse && lop <= OP_VAR) {  // f(leaf, top) as f_R(top, leaf)
+        x.w0 = (x.w0 & ~0xFFu) | reversed_op(g) | kFuse | (lop == OP_VAR ? kFuseVar : 0u);
+        x.w1 = l.w1;
+        row[out++] = x;
+        i = f2;
+      } else {
+        x.w0 = (x.w0 & ~0xFFu) | g;
+        row[out++] = x;
+        dstk[dsp++] = static_cast<uint16_t>(f2);
+        i = f1;
+      }
+      continue;
+    }
+    row[out++] = x;  // ternary: children in order, never reordered or fused
+    dstk[dsp++] = static_cast<uint16_t>(c2 + sz[c2]);
+    dstk[dsp++] = static_cast<uint16_t>(c2);
+    i = c1;
+  }
+  return out - 1;
+}
+
 // Leaf fusion: a unary/binary node whose first child (the next node in
 // prefix order) is a leaf absorbs that leaf — its payload moves into w1 and
 // the flags kFuse / kFuseVar are set. The interpreter then computes a binary
@@ -854,6 +993,14 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
       ti = stage_tree_warp(p, tp, s_nodes, lane);
       const Node* prog = s_nodes;
       if (ti.valid && ti.maxdepth - 1 > p.reorder_above) {
+        if (p.fuse) {  // reorder + fuse in one serial pass, straight into the row
+          int len = 0, dep = 0;
+          if (lane == 0) len = reorder_fuse_program(s_nodes, ti.len, row, scratch + (p.L + 1) * 8, p.L, true, &dep);
+          ti.len = __shfl_sync(FULL_MASK, len, 0);
+          ti.maxdepth = __shfl_sync(FULL_MASK, dep, 0);
+          __syncwarp();
+          goto compiled;
+        }
         ti.maxdepth = reorder_program(s_nodes, ti.len, s_reord, scratch + 2 * (p.L + 1) * 8, p.L, lane);
         prog = s_reord;
       }
@@ -867,6 +1014,7 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
     } else {
       ti = stage_tree_warp(p, tp, row, lane);
     }
+  compiled:
     if (lane == 0) {
       p.info[tp] = TreeMeta{ti.len, ti.valid ? ti.maxdepth : -1};
       if (!ti.valid) atomicOr(&p.ctl->flags, 1);
@@ -1065,7 +1213,12 @@ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 // Upper bound on the operand-stack depth of a well-formed row of length L:
 // one entry per leaf at most, and leaves <= (2L + 1) / 3 when arity >= 2.
 
-constexpr int kReorderMaxLen = 256;
+// every supported row length: the scratch is (L+1)*16 + 9L bytes per warp and
+// k_prepare sizes its CTA so the scratch fits (1 warp per CTA at L = 8192)
+constexpr int kReorderMaxLen = kMaxLenSupported;
+// levels of the per-warp private global stacks (rows deeper than every
+// shared-memory pass split and than this fall back to the locked pool)
+constexpr int kDeepPerWarpLevels = 32;
 
 template <int K, int MODE>
 const void* inter_fn() { return reinterpret_cast<const void*>(&k_inter<K, MODE>); }
@@ -1241,21 +1394,28 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   kp.prog_ld = prog_ld;
   // evaluation-order optimisation in the compile pass: single-output rows of
   // up to kReorderMaxLen nodes (shared scratch: nodes, reordered nodes, 4 u16 arrays + flags)
-  kp.reorder_scratch_bytes =
-      (!mode_multi(mode) && L <= kReorderMaxLen) ? static_cast<int32_t>(round_up(int64_t(L + 1) * 16 + 9 * L, 16)) : 0;
+  const bool can_compile = !mode_multi(mode) && L <= kReorderMaxLen;
+  bool reorder_on = can_compile, fuse_on = can_compile;
   if (const char* e = std::getenv("EVOGP_TUNE_REORDER")) {
-    if (std::atoi(e) == 0) kp.reorder_scratch_bytes = 0;
+    if (std::atoi(e) == 0) reorder_on = fuse_on = false;
   }
   // leaf fusion of single-output programs (measured: profiles/fuse_ab_r01.txt)
-  kp.fuse = kp.reorder_scratch_bytes > 0 ? 1 : 0;
+  if (const char* e = std::getenv("EVOGP_TUNE_FUSE")) {
+    if (std::atoi(e) == 0) fuse_on = false;
+  }
+  // shared scratch per compiling warp: decoded nodes + (fused) the one-pass
+  // reorder_fuse_program arrays, or (unfused) reorder_program's
+  kp.reorder_scratch_bytes =
+      !reorder_on ? 0
+                  : static_cast<int32_t>(fuse_on ? round_up(int64_t(L + 1) * 12 + 3 * L, 16)
+                                                 : round_up(int64_t(L + 1) * 16 + 9 * L, 16));
+  kp.fuse = fuse_on ? 1 : 0;
   kp.reorder_above = SD;
   if (const char* e = std::getenv("EVOGP_TUNE_REORDER_ABOVE")) kp.reorder_above = std::atoi(e) * SD;
-  if (const char* e = std::getenv("EVOGP_TUNE_FUSE")) {
-    if (std::atoi(e) == 0) kp.fuse = 0;
-  }
   kp.out_magic = static_cast<int32_t>((0x100000000ull + n_out - 1) / n_out);
   kp.deep_slots = deep_slots;
   kp.deep_slot_floats = deep_slot_floats;
+  kp.deep_pw_levels = std::min(depth, kDeepPerWarpLevels);
   // workspace layout (256-byte aligned sections)
   size_t off = 0;
   pl.off_ctl = off;
@@ -1270,6 +1430,9 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   off += round_up(static_cast<int64_t>(deep_slots) * 4, 256);
   pl.off_deep = off;
   off += round_up(static_cast<int64_t>(deep_slots) * per_slot, 256);
+  // per-warp private stacks: one per resident warp of the persistent grid
+  pl.off_deep_pw = off;
+  off += round_up(static_cast<int64_t>(grid) * warps * kp.deep_pw_levels * 32 * K * 4, 256);
   pl.off_prog = off;
   off += round_up(P * prog_ld * 8, 256);
   pl.off_info = off;
@@ -1285,9 +1448,25 @@ int launch(Plan& pl, int mode, const float* X, int32_t x_layout, const float* y,
   int launches = 0;
   {
     const int64_t total = static_cast<int64_t>(kp.n_in + 1) * kp.Dpad;
+    // warps per CTA such that their compile scratch fits the opt-in shared memory
+    const int wpb = kp.reorder_scratch_bytes > 0
+                        ? std::max(1, std::min(8, (220 * 1024) / kp.reorder_scratch_bytes))
+                        : 8;
+    const int threads = 32 * wpb;
+    const size_t psmem = static_cast<size_t>(wpb) * kp.reorder_scratch_bytes;
+    if (psmem > 48 * 1024) {
+      static thread_local int attr_dev = -1;
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (attr_dev != dev) {
+        cudaFuncSetAttribute(k_prepare, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr_dev = dev;
+      }
+    }
     const int64_t blocks = std::max<int64_t>(
-        1, std::min<int64_t>(std::max((total + 255) / 256, (kp.P + 7) / 8), static_cast<int64_t>(148) * 16));
-    k_prepare<<<static_cast<int>(blocks), 256, 8 * kp.reorder_scratch_bytes, s>>>(kp, X, x_layout,
+        1, std::min<int64_t>(std::max((total + threads - 1) / threads, (kp.P + wpb - 1) / wpb),
+                             static_cast<int64_t>(148) * 16 * (8 / wpb)));
+    k_prepare<<<static_cast<int>(blocks), threads, psmem, s>>>(kp, X, x_layout,
                                                                                  mode_reduce(mode) ? y : nullptr,
                                                         mode == MODE_CLS, mode_reduce(mode) ? kp.P : 0);
     ++launches;

@@ -129,6 +129,7 @@ class Config:
     modi_prob: float
     index: int
     paired: bool = False  # NEXT-2: D = observations per individual (B), each tree on its own
+    loop: bool = False  # NEXT-4: the whole generational loop (Algorithm 1), population generated on device
 
     @property
     def seed(self) -> int:
@@ -144,6 +145,11 @@ CONFIGS = {
     # NEXT-2: one control step of 10^6 policy trees, each on
     # its own 17-dim observation, 6 Modi outputs (shapes from config 5)
     "n2": Config("n2_paired_policy", 1_000_000, 63, 17, 6, 1, "normal", 0.0, 0.0, 0.1, 6, True),
+    # NEXT-4: the paper's whole-run GPops/s protocol at its
+    # peak cell (tab:gpops_summary P:592: P = 10^5, D = 392 Auto-MPG-shaped
+    # rows with 7 features, tab:sr_datasets P:550), max tree size 512 and the
+    # rest of tab:sr_params; synthetic Pagie-7 targets
+    "g1": Config("g1_sr_loop", 100_000, 512, 7, 1, 392, "uniform", -1.0, 1.0, 0.0, 7, False, True),
 }
 
 

@@ -695,3 +695,35 @@ def test_paired_edge_cases():
     with pytest.raises(evogp.EvogpError):
         evogp.eval_paired(tb, torch.zeros((1, big), device="cuda"), torch.zeros((1, big), dtype=torch.int16,
                           device="cuda"), torch.zeros((1, n_in), device="cuda"))
+
+
+@pytest.mark.parametrize("reorder", ["1", "0"])
+def test_long_rows_evolved_shapes(monkeypatch, reorder):
+    """max_len 512 (tab:sr_params P:475): generated GROW/FULL populations with
+    deep, unbalanced trees and 256-deep left combs, IEEE mix, both kernels,
+    with the compile pass's reordering on (shared stacks) and off (the global
+    deep-stack pool): bit-exact vs the FP32-faithful oracle."""
+    monkeypatch.setenv("EVOGP_TUNE_REORDER", reorder)
+    L, n_in, D = 512, 3, 300
+    cfg = dict(max_len=L, n_inputs=n_in, n_outputs=1, funcs=list(synth.M_IEEE), const_lo=-1.0, const_hi=1.0,
+               p_const=0.5, p_leaf=0.05, p_modi=0.0, depth_min=4, depth_max=12, tournament_size=2,
+               p_crossover=0.0, p_mutation=0.0, crossover_kind=0, leaf_bias=0.1, mutation_weights=[1] + [0] * 7,
+               point_rate=0.1, const_sigma=0.1, subtree_depth=4)
+    t, v, s = oracle.generate(200, cfg, 31)
+    for i in range(0, 200, 10):  # left combs of ADD/SUB: depth 256 without reordering
+        n = 511
+        t[i, :255] = 3
+        v[i, :255] = np.where(np.arange(255) % 2 == 0, 0.0, 1.0)
+        t[i, 255:n] = 1
+        v[i, 255:n] = np.arange(256) % n_in
+        t[i, n:] = -1
+        v[i, n:] = np.nan
+        lens = np.concatenate([[0], [n]])
+        _, _, ss = oracle.tensorize(lens, t[i, :n], v[i, :n], L, n_in, 1)
+        s[i] = ss[0]
+    X = synth.dataset_X(12, 0, D, n_in, lo=0.5, hi=1.5)
+    r32 = oracle.evaluate(t, v, s, X, mode=1)[:, :, 0]
+    dev = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (t, v, s)]
+    for strategy in ("inter", "intra"):
+        g = gpu_eval(dev, X, 1, strategy)[:, :, 0]
+        assert same_bits_mod_zero(g, r32).all(), strategy
