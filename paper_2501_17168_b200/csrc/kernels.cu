@@ -805,6 +805,123 @@ __device__ int reorder_program(const Node* s_nodes, int n, Node* row, unsigned c
   return depth;
 }
 
+// Warp-parallel Sethi-Ullman reordering (same decisions as reorder_program)
+// for rows whose caller-provided subtree sizes are consistent — always the
+// case for rows made by evogp_tensorize / evogp_reproduce; checked here in
+// parallel: a leaf has size 1 and walking a node's children by their sizes
+// ends exactly at i + size[i] (by induction from the last node this makes
+// every size the true one). Lanes own 32 consecutive nodes:
+//  * needs bottom-up, chunks from the last to the first; inside a chunk the
+//    lanes iterate until every node's children are known (in-chunk nesting
+//    depth iterations; children in later chunks are final);
+//  * new positions top-down: np[j] = j + acc[j], acc[j] = acc[parent] +
+//    (parent swapped ? (j first child ? +size(second) : -size(first)) : 0),
+//    chunks from the first, iterating inside a chunk the same way;
+//  * scatter into s_reord (opcode reversed on swapped nodes).
+// Returns the row's stack need, or -1 when the sizes are inconsistent (the
+// caller then uses the serial path). Scratch: 9 L bytes.
+__device__ int reorder_program_par(const Node* s_nodes, int n, const int16_t* __restrict__ urow_size, Node* s_reord,
+                                   unsigned char* scr, int L, int lane) {
+  uint16_t* sz = reinterpret_cast<uint16_t*>(scr);
+  uint16_t* nd = sz + L;
+  uint16_t* par = nd + L;
+  int16_t* acc = reinterpret_cast<int16_t*>(par + L);
+  uint8_t* sw = reinterpret_cast<uint8_t*>(acc + L);
+  for (int i = lane; i < n; i += 32) {
+    const int v = __ldg(urow_size + i);
+    sz[i] = static_cast<uint16_t>(v < 1 || v > n - i ? 0 : v);
+    sw[i] = 0;
+  }
+  __syncwarp();
+  bool ok = true;
+  for (int i = lane; i < n; i += 32) {
+    const uint32_t op = s_nodes[i + 1].w0 & 0xFFu;
+    const int ar = op <= OP_VAR ? 0 : func_arity(static_cast<int>(op) - OP_FN);
+    const int si = sz[i];
+    int c = i + 1, q = 0;
+    for (; q < ar && c < n; ++q) {
+      par[c] = static_cast<uint16_t>(i);
+      const int sc = sz[c];
+      c = sc ? c + sc : n + 1;
+    }
+    ok = ok && si != 0 && (ar == 0 ? si == 1 : (q == ar && c == i + si));
+  }
+  if (!__all_sync(FULL_MASK, ok) || sz[0] != n) return -1;
+  __syncwarp();
+  // bottom-up needs
+  const int nblk = (n + 31) >> 5;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int i = b * 32 + lane;
+    int ar = 0, c1 = 0, c2 = 0, c3 = 0, q = 1;
+    if (i < n) {
+      const uint32_t op = s_nodes[i + 1].w0 & 0xFFu;
+      ar = op <= OP_VAR ? 0 : func_arity(static_cast<int>(op) - OP_FN);
+      c1 = i + 1;
+      if (ar >= 2) c2 = c1 + sz[c1];
+      if (ar == 3) c3 = c2 + sz[c2];
+      q = ar == 0 ? 1 : 0;
+      nd[i] = static_cast<uint16_t>(q);
+    }
+    __syncwarp();
+    while (!__all_sync(FULL_MASK, i >= n || q != 0)) {
+      if (i < n && q == 0) {
+        const int n1 = nd[c1], n2 = ar >= 2 ? nd[c2] : 1, n3 = ar == 3 ? nd[c3] : 1;
+        if (n1 && n2 && n3) {
+          if (ar == 1) {
+            q = n1;
+          } else if (ar == 2) {
+            const int q_def = max(n2, n1 + 1), q_swp = max(n1, n2 + 1);
+            sw[i] = q_swp < q_def;
+            q = min(q_def, q_swp);
+          } else {
+            q = max(n3, max(n2 + 1, n1 + 2));
+          }
+        }
+      }
+      __syncwarp();
+      if (i < n && q) nd[i] = static_cast<uint16_t>(q);
+      __syncwarp();
+    }
+  }
+  const int depth = nd[0];
+  // top-down positions
+  constexpr int16_t kUnknown = INT16_MIN;
+  for (int b = 0; b < nblk; ++b) {
+    const int j = b * 32 + lane;
+    int a = kUnknown, off = 0, pj = 0;
+    if (j < n) {
+      if (j == 0) {
+        a = 0;
+      } else {
+        pj = par[j];
+        if (sw[pj]) {
+          const int f = pj + 1, sc = f + sz[f];
+          off = j == f ? sz[sc] : -static_cast<int>(sz[f]);
+        }
+      }
+      acc[j] = static_cast<int16_t>(a);
+    }
+    __syncwarp();
+    while (!__all_sync(FULL_MASK, j >= n || a != kUnknown)) {
+      if (j < n && a == kUnknown) {
+        const int ap = acc[pj];
+        if (ap != kUnknown) a = ap + off;
+      }
+      __syncwarp();
+      if (j < n && a != kUnknown) acc[j] = static_cast<int16_t>(a);
+      __syncwarp();
+    }
+  }
+  for (int j = lane; j < n; j += 32) {
+    Node x = s_nodes[j + 1];
+    if (sw[j]) x.w0 = (x.w0 & ~0xFFu) | reversed_op(x.w0 & 0xFFu);
+    s_reord[j + acc[j] + 1] = x;
+  }
+  if (lane == 0) s_reord[0] = s_nodes[0];
+  __syncwarp();
+  return depth;
+}
+
 // Reordering + leaf fusion in one pass for deep single-output rows (lane 0):
 //  1. reverse scan with a stack of packed (size << 16 | need) entries, the
 //     top entry in a register: subtree sizes, Sethi-Ullman needs and the
@@ -993,11 +1110,21 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
       ti = stage_tree_warp(p, tp, s_nodes, lane);
       const Node* prog = s_nodes;
       if (ti.valid && ti.maxdepth - 1 > p.reorder_above) {
-        if (p.fuse) {  // reorder + fuse in one serial pass, straight into the row
-          int len = 0, dep = 0;
-          if (lane == 0) len = reorder_fuse_program(s_nodes, ti.len, row, scratch + (p.L + 1) * 8, p.L, true, &dep);
+        if (p.fuse) {
+          // warp-parallel reorder into s_reord, then the warp-parallel fusion
+          const int dep = reorder_program_par(s_nodes, ti.len, p.size + tp * p.ld, s_reord,
+                                              scratch + 2 * (p.L + 1) * 8, p.L, lane);
+          if (dep > 0) {
+            ti.maxdepth = dep;
+            ti.len = fuse_copy(s_reord, ti.len, row, lane);
+            goto compiled;
+          }
+          // inconsistent caller sizes: reorder + fuse in one serial pass
+          int len = 0;
+          int dep2 = 0;
+          if (lane == 0) len = reorder_fuse_program(s_nodes, ti.len, row, scratch + (p.L + 1) * 8, p.L, true, &dep2);
           ti.len = __shfl_sync(FULL_MASK, len, 0);
-          ti.maxdepth = __shfl_sync(FULL_MASK, dep, 0);
+          ti.maxdepth = __shfl_sync(FULL_MASK, dep2, 0);
           __syncwarp();
           goto compiled;
         }
@@ -1403,12 +1530,11 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   if (const char* e = std::getenv("EVOGP_TUNE_FUSE")) {
     if (std::atoi(e) == 0) fuse_on = false;
   }
-  // shared scratch per compiling warp: decoded nodes + (fused) the one-pass
-  // reorder_fuse_program arrays, or (unfused) reorder_program's
+  // shared scratch per compiling warp: decoded nodes, reordered nodes and the
+  // per-node arrays of reorder_program(_par) (reorder_fuse_program needs less)
   kp.reorder_scratch_bytes =
       !reorder_on ? 0
-                  : static_cast<int32_t>(fuse_on ? round_up(int64_t(L + 1) * 12 + 3 * L, 16)
-                                                 : round_up(int64_t(L + 1) * 16 + 9 * L, 16));
+                  : static_cast<int32_t>(round_up(int64_t(L + 1) * 16 + 9 * L, 16));
   kp.fuse = fuse_on ? 1 : 0;
   kp.reorder_above = SD;
   if (const char* e = std::getenv("EVOGP_TUNE_REORDER_ABOVE")) kp.reorder_above = std::atoi(e) * SD;

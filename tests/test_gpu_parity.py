@@ -727,3 +727,26 @@ def test_long_rows_evolved_shapes(monkeypatch, reorder):
     for strategy in ("inter", "intra"):
         g = gpu_eval(dev, X, 1, strategy)[:, :, 0]
         assert same_bits_mod_zero(g, r32).all(), strategy
+
+
+def test_inconsistent_sizes_use_serial_compile_path():
+    """Only size[0] is part of the evaluation contract: rows whose other
+    size entries are wrong (the warp-parallel reorder's size check fails)
+    take the serial compile path and still evaluate bit-exactly."""
+    L, n_in, D = 255, 3, 200
+    cfg = dict(max_len=L, n_inputs=n_in, n_outputs=1, funcs=list(synth.M_IEEE), const_lo=-1.0, const_hi=1.0,
+               p_const=0.5, p_leaf=0.05, p_modi=0.0, depth_min=5, depth_max=10, tournament_size=2,
+               p_crossover=0.0, p_mutation=0.0, crossover_kind=0, leaf_bias=0.1, mutation_weights=[1] + [0] * 7,
+               point_rate=0.1, const_sigma=0.1, subtree_depth=4)
+    t, v, s = oracle.generate(300, cfg, 41)
+    X = synth.dataset_X(13, 0, D, n_in, lo=0.5, hi=1.5)
+    r32 = oracle.evaluate(t, v, s, X, mode=1)[:, :, 0]
+    s_bad = s.copy()
+    long_rows = s[:, 0] > 2
+    s_bad[long_rows, 1] = 1  # wrong (unless node 1 is a leaf) but size[0] intact
+    s_bad[long_rows, 2] = s[long_rows, 0]
+    for sizes in (s, s_bad):
+        dev = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (t, v, sizes)]
+        for strategy in ("inter", "intra"):
+            g = gpu_eval(dev, X, 1, strategy)[:, :, 0]
+            assert same_bits_mod_zero(g, r32).all(), strategy
