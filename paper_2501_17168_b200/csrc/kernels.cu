@@ -805,32 +805,40 @@ __device__ int reorder_program(const Node* s_nodes, int n, Node* row, unsigned c
   return depth;
 }
 
-// Warp-parallel Sethi-Ullman reordering (same decisions as reorder_program)
-// for rows whose caller-provided subtree sizes are consistent — always the
-// case for rows made by evogp_tensorize / evogp_reproduce; checked here in
-// parallel: a leaf has size 1 and walking a node's children by their sizes
-// ends exactly at i + size[i] (by induction from the last node this makes
-// every size the true one). Lanes own 32 consecutive nodes:
-//  * needs bottom-up, chunks from the last to the first; inside a chunk the
-//    lanes iterate until every node's children are known (in-chunk nesting
-//    depth iterations; children in later chunks are final);
+// Warp-parallel Sethi-Ullman reordering + leaf fusion of a single-output
+// row, written straight into its program row (same decisions as
+// reorder_program followed by fuse_copy). Used when the caller's subtree
+// sizes are consistent — always the case for rows made by evogp_tensorize /
+// evogp_reproduce; checked here in parallel: a leaf has size 1 and walking a
+// node's children by their sizes ends exactly at i + size[i] (by induction
+// from the last node this makes every size the true one). Lanes own 32
+// consecutive nodes:
+//  * needs bottom-up, chunks from the last to the first: in-chunk children
+//    are read by shuffles, iterating until every node is known (children in
+//    later chunks are final, in shared memory);
 //  * new positions top-down: np[j] = j + acc[j], acc[j] = acc[parent] +
-//    (parent swapped ? (j first child ? +size(second) : -size(first)) : 0),
-//    chunks from the first, iterating inside a chunk the same way;
-//  * scatter into s_reord (opcode reversed on swapped nodes).
-// Returns the row's stack need, or -1 when the sizes are inconsistent (the
-// caller then uses the serial path). Scratch: 9 L bytes.
-__device__ int reorder_program_par(const Node* s_nodes, int n, const int16_t* __restrict__ urow_size, Node* s_reord,
-                                   unsigned char* scr, int L, int lane) {
+//    (parent swapped ? (j first child ? +size(second) : -size(first)) : 0):
+//    pointer jumping over in-chunk parents by shuffles (5 rounds), chunks
+//    from the first;
+//  * fusion: a unary / binary node absorbs its first-visited child when that
+//    is a leaf that is not the last node; positions are compacted by a
+//    prefix count of the absorbed leaves over new positions;
+//  * scatter of the final words to the global row.
+// Returns the new length (and *depth_out), or -1 when the sizes are
+// inconsistent. Scratch after the decoded nodes: 10 L bytes.
+__device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __restrict__ urow_size, Node* row,
+                                unsigned char* scr, int L, int lane, int* depth_out) {
   uint16_t* sz = reinterpret_cast<uint16_t*>(scr);
-  uint16_t* nd = sz + L;
+  uint16_t* nd = sz + L;  // needs; later the absorbed-prefix counts by new position
   uint16_t* par = nd + L;
   int16_t* acc = reinterpret_cast<int16_t*>(par + L);
   uint8_t* sw = reinterpret_cast<uint8_t*>(acc + L);
+  uint8_t* absd = sw + L;  // an absorbed leaf sits at new position q
   for (int i = lane; i < n; i += 32) {
     const int v = __ldg(urow_size + i);
     sz[i] = static_cast<uint16_t>(v < 1 || v > n - i ? 0 : v);
     sw[i] = 0;
+    absd[i] = 0;
   }
   __syncwarp();
   bool ok = true;
@@ -848,178 +856,141 @@ __device__ int reorder_program_par(const Node* s_nodes, int n, const int16_t* __
   }
   if (!__all_sync(FULL_MASK, ok) || sz[0] != n) return -1;
   __syncwarp();
-  // bottom-up needs
   const int nblk = (n + 31) >> 5;
+  // ---- bottom-up needs
   for (int b = nblk - 1; b >= 0; --b) {
-    const int i = b * 32 + lane;
-    int ar = 0, c1 = 0, c2 = 0, c3 = 0, q = 1;
+    const int base = b * 32, i = base + lane;
+    int ar = 0, q = 1, l1 = lane, l2 = lane, l3 = lane, v1 = 1, v2 = 1, v3 = 1;
     if (i < n) {
       const uint32_t op = s_nodes[i + 1].w0 & 0xFFu;
       ar = op <= OP_VAR ? 0 : func_arity(static_cast<int>(op) - OP_FN);
-      c1 = i + 1;
-      if (ar >= 2) c2 = c1 + sz[c1];
-      if (ar == 3) c3 = c2 + sz[c2];
       q = ar == 0 ? 1 : 0;
-      nd[i] = static_cast<uint16_t>(q);
+      if (ar >= 1) {
+        const int c1 = i + 1;
+        if (c1 < base + 32) l1 = c1 - base, v1 = 0;
+        else v1 = nd[c1];
+        if (ar >= 2) {
+          const int c2 = c1 + sz[c1];
+          if (c2 < base + 32) l2 = c2 - base, v2 = 0;
+          else v2 = nd[c2];
+          if (ar == 3) {
+            const int c3 = c2 + sz[c2];
+            if (c3 < base + 32) l3 = c3 - base, v3 = 0;
+            else v3 = nd[c3];
+          }
+        }
+      }
     }
-    __syncwarp();
-    while (!__all_sync(FULL_MASK, i >= n || q != 0)) {
-      if (i < n && q == 0) {
-        const int n1 = nd[c1], n2 = ar >= 2 ? nd[c2] : 1, n3 = ar == 3 ? nd[c3] : 1;
+    uint8_t swp = 0;
+    while (!__all_sync(FULL_MASK, q != 0)) {
+      const int x1 = __shfl_sync(FULL_MASK, q, l1);
+      const int x2 = __shfl_sync(FULL_MASK, q, l2);
+      const int x3 = __shfl_sync(FULL_MASK, q, l3);
+      if (q == 0) {
+        const int n1 = v1 ? v1 : x1, n2 = v2 ? v2 : x2, n3 = v3 ? v3 : x3;
         if (n1 && n2 && n3) {
           if (ar == 1) {
             q = n1;
           } else if (ar == 2) {
             const int q_def = max(n2, n1 + 1), q_swp = max(n1, n2 + 1);
-            sw[i] = q_swp < q_def;
+            swp = q_swp < q_def;
             q = min(q_def, q_swp);
           } else {
             q = max(n3, max(n2 + 1, n1 + 2));
           }
         }
       }
-      __syncwarp();
-      if (i < n && q) nd[i] = static_cast<uint16_t>(q);
-      __syncwarp();
     }
-  }
-  const int depth = nd[0];
-  // top-down positions
-  constexpr int16_t kUnknown = INT16_MIN;
-  for (int b = 0; b < nblk; ++b) {
-    const int j = b * 32 + lane;
-    int a = kUnknown, off = 0, pj = 0;
-    if (j < n) {
-      if (j == 0) {
-        a = 0;
-      } else {
-        pj = par[j];
-        if (sw[pj]) {
-          const int f = pj + 1, sc = f + sz[f];
-          off = j == f ? sz[sc] : -static_cast<int>(sz[f]);
-        }
-      }
-      acc[j] = static_cast<int16_t>(a);
+    if (i < n) {
+      nd[i] = static_cast<uint16_t>(q);
+      sw[i] = swp;
     }
     __syncwarp();
-    while (!__all_sync(FULL_MASK, j >= n || a != kUnknown)) {
-      if (j < n && a == kUnknown) {
-        const int ap = acc[pj];
-        if (ap != kUnknown) a = ap + off;
-      }
-      __syncwarp();
-      if (j < n && a != kUnknown) acc[j] = static_cast<int16_t>(a);
-      __syncwarp();
-    }
   }
+  *depth_out = nd[0];
+  // ---- top-down positions (pointer jumping inside a chunk)
+  for (int b = 0; b < nblk; ++b) {
+    const int base = b * 32, j = base + lane;
+    int a = 0, ptr = -1;
+    if (j < n && j > 0) {
+      const int pj = par[j];
+      int off = 0;
+      if (sw[pj]) {
+        const int f = pj + 1;
+        off = j == f ? static_cast<int>(sz[f + sz[f]]) : -static_cast<int>(sz[f]);
+      }
+      if (pj < base) {
+        a = acc[pj] + off;
+      } else {
+        a = off;
+        ptr = pj - base;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      const int src = ptr >= 0 ? ptr : lane;
+      const int ap = __shfl_sync(FULL_MASK, a, src);
+      const int pp = __shfl_sync(FULL_MASK, ptr, src);
+      if (ptr >= 0) {
+        a += ap;
+        ptr = pp;
+      }
+    }
+    if (j < n) acc[j] = static_cast<int16_t>(a);
+    __syncwarp();
+  }
+  // ---- fusion decisions: absorbed leaves marked at their new positions
   for (int j = lane; j < n; j += 32) {
-    Node x = s_nodes[j + 1];
-    if (sw[j]) x.w0 = (x.w0 & ~0xFFu) | reversed_op(x.w0 & 0xFFu);
-    s_reord[j + acc[j] + 1] = x;
-  }
-  if (lane == 0) s_reord[0] = s_nodes[0];
-  __syncwarp();
-  return depth;
-}
-
-// Reordering + leaf fusion in one pass for deep single-output rows (lane 0):
-//  1. reverse scan with a stack of packed (size << 16 | need) entries, the
-//     top entry in a register: subtree sizes, Sethi-Ullman needs and the
-//     swap decision of every binary node (same rule as reorder_program);
-//  2. depth-first emission in the new prefix order (swapped binary nodes
-//     visit their second child first and take the reversed opcode), fusing a
-//     leaf that is the first-visited child of a unary / binary node (same
-//     rule as fuse_copy, applied to the reordered order), straight into the
-//     program row. Returns the new length; *depth = the row's stack need.
-// Scratch: 4 (L + 1) + 3 L bytes after the decoded nodes.
-__device__ int reorder_fuse_program(const Node* s_nodes, int n, Node* row, unsigned char* scr, int L, bool fuse,
-                                    int* depth) {
-  uint32_t* stk = reinterpret_cast<uint32_t*>(scr);       // L + 1 entries
-  uint16_t* sz = reinterpret_cast<uint16_t*>(stk + L + 1);  // subtree sizes
-  uint8_t* sw = reinterpret_cast<uint8_t*>(sz + L);         // swapped
-  int sp = 0;
-  uint32_t topv = 0;
-  for (int i = n - 1; i >= 0; --i) {
-    const uint32_t op = s_nodes[i + 1].w0 & 0xFFu;
-    const int ar = op <= OP_VAR ? 0 : func_arity(static_cast<int>(op) - OP_FN);
-    uint32_t r;
-    uint8_t swp = 0;
-    if (ar == 0) {
-      stk[sp++] = topv;
-      r = (1u << 16) | 1u;
-    } else if (ar == 1) {
-      r = topv + (1u << 16);
-    } else if (ar == 2) {
-      const uint32_t a = topv, b = stk[--sp];  // a = leftmost child (first pop)
-      const int qa = a & 0xFFFF, qb = b & 0xFFFF;
-      const int q_def = max(qb, qa + 1), q_swp = max(qa, qb + 1);
-      swp = q_swp < q_def;
-      r = ((1u + (a >> 16) + (b >> 16)) << 16) | static_cast<uint32_t>(swp ? q_swp : q_def);
-    } else {
-      const uint32_t a = topv, b = stk[--sp], c = stk[--sp];
-      const int q = max(static_cast<int>(c & 0xFFFF), max(static_cast<int>(b & 0xFFFF) + 1,
-                                                           static_cast<int>(a & 0xFFFF) + 2));
-      r = ((1u + (a >> 16) + (b >> 16) + (c >> 16)) << 16) | static_cast<uint32_t>(q);
-    }
-    topv = r;
-    sz[i] = static_cast<uint16_t>(r >> 16);
-    sw[i] = swp;
-  }
-  *depth = static_cast<int>(topv & 0xFFFF);
-  uint16_t* dstk = reinterpret_cast<uint16_t*>(stk);  // the scan stack is dead now
-  int out = 1, dsp = 0, i = 0;
-  row[0] = s_nodes[0];
-  for (;;) {
-    Node x = s_nodes[i + 1];
-    const uint32_t op = x.w0 & 0xFFu;
-    if (op <= OP_VAR) {
-      row[out++] = x;
-      if (dsp == 0) break;
-      i = dstk[--dsp];
-      continue;
-    }
+    const uint32_t op = s_nodes[j + 1].w0 & 0xFFu;
+    if (op <= OP_VAR) continue;
     const int ar = func_arity(static_cast<int>(op) - OP_FN);
-    const int c1 = i + 1;
-    if (ar == 1) {
-      const Node l = s_nodes[c1 + 1];
-      const uint32_t lop = l.w0 & 0xFFu;
-      if (fuse && lop <= OP_VAR && dsp > 0) {  // never absorb the last node
-        x.w0 = (x.w0 & ~0xFFu) | op | kFuse | (lop == OP_VAR ? kFuseVar : 0u);
-        x.w1 = l.w1;
-        row[out++] = x;
-        i = dstk[--dsp];
-      } else {
-        row[out++] = x;
-        i = c1;
-      }
-      continue;
-    }
-    const int c2 = c1 + sz[c1];
-    if (ar == 2) {
-      const bool swp = sw[i] != 0;
-      const uint32_t g = swp ? reversed_op(op) : op;
-      const int f1 = swp ? c2 : c1, f2 = swp ? c1 : c2;
-      const Node l = s_nodes[f1 + 1];
-      const uint32_t lop = l.w0 & 0xFFu;
-      if (fuse && lop <= OP_VAR) {  // f(leaf, top) as f_R(top, leaf)
-        x.w0 = (x.w0 & ~0xFFu) | reversed_op(g) | kFuse | (lop == OP_VAR ? kFuseVar : 0u);
-        x.w1 = l.w1;
-        row[out++] = x;
-        i = f2;
-      } else {
-        x.w0 = (x.w0 & ~0xFFu) | g;
-        row[out++] = x;
-        dstk[dsp++] = static_cast<uint16_t>(f2);
-        i = f1;
-      }
-      continue;
-    }
-    row[out++] = x;  // ternary: children in order, never reordered or fused
-    dstk[dsp++] = static_cast<uint16_t>(c2 + sz[c2]);
-    dstk[dsp++] = static_cast<uint16_t>(c2);
-    i = c1;
+    if (ar > 2) continue;
+    const int c1 = j + 1;
+    const int f1 = (ar == 2 && sw[j]) ? c1 + sz[c1] : c1;
+    if ((s_nodes[f1 + 1].w0 & 0xFFu) > OP_VAR) continue;
+    const int pos = f1 + acc[f1];
+    if (pos != n - 1) absd[pos] = 1;
   }
-  return out - 1;
+  __syncwarp();
+  // exclusive prefix count of the absorbed positions -> nd[q]
+  int carry = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int q = base + lane;
+    const bool f = q < n && absd[q];
+    const unsigned m = __ballot_sync(FULL_MASK, f);
+    if (q < n) nd[q] = static_cast<uint16_t>(carry + __popc(m & ((1u << lane) - 1u)));
+    carry += __popc(m);
+  }
+  __syncwarp();
+  // ---- scatter the final words
+  for (int j = lane; j < n; j += 32) {
+    const int pos = j + acc[j];
+    if (absd[pos]) continue;  // an absorbed leaf
+    Node x = s_nodes[j + 1];
+    const uint32_t op = x.w0 & 0xFFu;
+    if (op > OP_VAR) {
+      const int ar = func_arity(static_cast<int>(op) - OP_FN);
+      const bool swp = ar == 2 && sw[j];
+      uint32_t g = swp ? reversed_op(op) : op;
+      if (ar <= 2) {
+        const int c1 = j + 1;
+        const int f1 = swp ? c1 + sz[c1] : c1;
+        if (absd[f1 + acc[f1]] && (s_nodes[f1 + 1].w0 & 0xFFu) <= OP_VAR) {
+          // f(leaf, top) as f_R(top, leaf); a unary node keeps its op
+          const Node l = s_nodes[f1 + 1];
+          if (ar == 2) g = reversed_op(g);
+          x.w0 = (x.w0 & ~0xFFu) | g | kFuse | ((l.w0 & 0xFFu) == OP_VAR ? kFuseVar : 0u);
+          x.w1 = l.w1;
+        } else {
+          x.w0 = (x.w0 & ~0xFFu) | g;
+        }
+      }
+    }
+    row[pos - nd[pos] + 1] = x;
+  }
+  if (lane == 0) row[0] = s_nodes[0];
+  __syncwarp();
+  return n - carry;
 }
 
 // Leaf fusion: a unary/binary node whose first child (the next node in
@@ -1111,25 +1082,20 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
       const Node* prog = s_nodes;
       if (ti.valid && ti.maxdepth - 1 > p.reorder_above) {
         if (p.fuse) {
-          // warp-parallel reorder into s_reord, then the warp-parallel fusion
-          const int dep = reorder_program_par(s_nodes, ti.len, p.size + tp * p.ld, s_reord,
-                                              scratch + 2 * (p.L + 1) * 8, p.L, lane);
-          if (dep > 0) {
+          // warp-parallel reorder + fusion straight into the program row; rows
+          // with inconsistent caller sizes are fused without reordering
+          int dep = 0;
+          const int len = reorder_fuse_par(s_nodes, ti.len, p.size + tp * p.ld, row, scratch + (p.L + 1) * 8, p.L,
+                                           lane, &dep);
+          if (len > 0) {
+            ti.len = len;
             ti.maxdepth = dep;
-            ti.len = fuse_copy(s_reord, ti.len, row, lane);
             goto compiled;
           }
-          // inconsistent caller sizes: reorder + fuse in one serial pass
-          int len = 0;
-          int dep2 = 0;
-          if (lane == 0) len = reorder_fuse_program(s_nodes, ti.len, row, scratch + (p.L + 1) * 8, p.L, true, &dep2);
-          ti.len = __shfl_sync(FULL_MASK, len, 0);
-          ti.maxdepth = __shfl_sync(FULL_MASK, dep2, 0);
-          __syncwarp();
-          goto compiled;
+        } else {
+          ti.maxdepth = reorder_program(s_nodes, ti.len, s_reord, scratch + 2 * (p.L + 1) * 8, p.L, lane);
+          prog = s_reord;
         }
-        ti.maxdepth = reorder_program(s_nodes, ti.len, s_reord, scratch + 2 * (p.L + 1) * 8, p.L, lane);
-        prog = s_reord;
       }
       if (ti.valid && p.fuse) {
         ti.len = fuse_copy(prog, ti.len, row, lane);
@@ -1530,11 +1496,12 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   if (const char* e = std::getenv("EVOGP_TUNE_FUSE")) {
     if (std::atoi(e) == 0) fuse_on = false;
   }
-  // shared scratch per compiling warp: decoded nodes, reordered nodes and the
-  // per-node arrays of reorder_program(_par) (reorder_fuse_program needs less)
+  // shared scratch per compiling warp: decoded nodes + reorder_fuse_par's
+  // arrays, or (unfused) reordered nodes + reorder_program's arrays
   kp.reorder_scratch_bytes =
       !reorder_on ? 0
-                  : static_cast<int32_t>(round_up(int64_t(L + 1) * 16 + 9 * L, 16));
+                  : static_cast<int32_t>(fuse_on ? round_up(int64_t(L + 1) * 8 + 10 * L, 16)
+                                                 : round_up(int64_t(L + 1) * 16 + 9 * L, 16));
   kp.fuse = fuse_on ? 1 : 0;
   kp.reorder_above = SD;
   if (const char* e = std::getenv("EVOGP_TUNE_REORDER_ABOVE")) kp.reorder_above = std::atoi(e) * SD;

@@ -729,10 +729,10 @@ def test_long_rows_evolved_shapes(monkeypatch, reorder):
         assert same_bits_mod_zero(g, r32).all(), strategy
 
 
-def test_inconsistent_sizes_use_serial_compile_path():
+def test_inconsistent_sizes_skip_reordering():
     """Only size[0] is part of the evaluation contract: rows whose other
     size entries are wrong (the warp-parallel reorder's size check fails)
-    take the serial compile path and still evaluate bit-exactly."""
+    are compiled without reordering and still evaluate bit-exactly."""
     L, n_in, D = 255, 3, 200
     cfg = dict(max_len=L, n_inputs=n_in, n_outputs=1, funcs=list(synth.M_IEEE), const_lo=-1.0, const_hi=1.0,
                p_const=0.5, p_leaf=0.05, p_modi=0.0, depth_min=5, depth_max=10, tournament_size=2,
