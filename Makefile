@@ -6,7 +6,7 @@ LIB := $(PKG)/libevogp.so
 # IEEE-faithful FP32 on the parity path: no fast math, no FTZ, IEEE div/sqrt (R5)
 NVFLAGS := -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
            -ftz=false -prec-div=true -prec-sqrt=true -Xcompiler -fPIC,-O2 -Xptxas -v
-SRCS := $(CSRC)/kernels.cu $(CSRC)/paired.cu $(CSRC)/variation.cu $(CSRC)/capi.cu $(CSRC)/tensorize.cpp
+SRCS := $(CSRC)/kernels.cu $(CSRC)/paired.cu $(CSRC)/variation.cu $(CSRC)/tensorize_dev.cu $(CSRC)/capi.cu $(CSRC)/tensorize.cpp
 HDRS := $(CSRC)/evogp_internal.h $(CSRC)/fastmath.cuh $(CSRC)/decode.cuh $(CSRC)/selector_table.inc include/evogp.h
 
 all: $(LIB) oracle/liboracle.so synth/libsynth.so

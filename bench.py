@@ -9,8 +9,10 @@ A step is one pass of the whole hot path over one batch: dataset staging
 the fused FP64 SSE/MSE (a7) — or the multi-output store (a6) for c5 — and,
 for N > 1, the NCCL combine (a8). GPops/s = sum_p len_p * D / t (PAPER.md
 P:600-605 with the factor D the tables need, reading R10). Tensorizing
-(a1) is timed in the `e2e` leg only (host prefix lists -> public API ->
-host result), together with the host<->device copies.
+(a1) is timed in the `e2e` leg only: the prefix lists are copied from pinned
+host memory, tensorized on the device (evogp_tensorize_device), then the
+hot path runs and its result is read back. `--config g1` times the whole
+generational loop instead (NEXT-4).
 
 Timing: W warm-up steps, then K steps each bracketed by CUDA events on the
 launching stream; L2 is flushed (256 MiB write) before every timed step,
@@ -590,19 +592,22 @@ def main():
     # ---- e2e: host prefix lists -> tensorize -> H2D -> device call -> D2H
     e2e = None
     if not args.no_e2e:
-        pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
-        h_t, h_v, h_s = pin(np.empty_like(t)), pin(np.empty_like(v)), pin(np.empty_like(s))
+        # the caller's prefix lists (CSR) in pinned memory -> H2D -> tensorized
+        # on the device (evogp_tensorize_device, row a1) -> hot path -> D2H
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        h_off, h_ty, h_va = pin(pt.offsets.astype(np.int64)), pin(pt.types), pin(pt.values)
+        d_off, d_ty, d_va = (torch.empty_like(x, device=dev) for x in (h_off, h_ty, h_va))
         h_X, h_y = pin(X), pin(y)
         res_len = P_total if (cfg.n_out == 1) else P_local * D_local * cfg.n_out
         h_res = torch.empty(res_len, dtype=torch.float64 if cfg.n_out == 1 else torch.float32).pin_memory()
-        h2d = sum(x.numel() * x.element_size() for x in (h_t, h_v, h_s, h_X, h_y))
+        h2d = sum(x.numel() * x.element_size() for x in (h_off, h_ty, h_va, h_X, h_y))
         d2h = h_res.numel() * h_res.element_size()
 
         def e2e_step():
-            evogp.tensorize(pt.offsets, pt.types, pt.values, cfg.max_len, cfg.n_in, cfg.n_out,
-                            out=(h_t.numpy(), h_v.numpy(), h_s.numpy()))
-            for dst, src in ((td, h_t), (vd, h_v), (sd, h_s), (Xd, h_X), (yd, h_y)):
+            for dst, src in ((d_off, h_off), (d_ty, h_ty), (d_va, h_va), (Xd, h_X), (yd, h_y)):
                 dst.copy_(src, non_blocking=True)
+            evogp.tensorize_device(d_off, d_ty, d_va, cfg.max_len, cfg.n_in, cfg.n_out, out=(td, vd, sd),
+                                   status=False)
             r = step()
             h_res.copy_(r.reshape(-1), non_blocking=True)
             torch.cuda.current_stream().synchronize()
@@ -618,7 +623,9 @@ def main():
         if world > 1:
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
         e2e = {"value": total_work * args.steps / el.item(), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "includes": "host tensorize (a1) + H2D + hot path + D2H"}
+               "d2h_bytes_per_step": int(d2h),
+               "includes": "H2D of the prefix lists (CSR) + X + y from pinned memory, device tensorize (a1), "
+                           "hot path, D2H of the result"}
 
     if rank == 0:
         peaks, peak_src = measured_peaks()

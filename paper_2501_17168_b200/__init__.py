@@ -22,7 +22,7 @@ from ._lib import (E_ARG, E_CUDA, E_FUNC_UNKNOWN, E_MALFORMED, E_OUT_RANGE, E_TO
 _LIB = _lib.load()
 
 __all__ = [
-    "tensorize", "eval", "sr_fitness", "sr_sse", "classification_accuracy", "eval_paired", "select_strategy", "workspace_size", "Workspace",
+    "tensorize", "tensorize_device", "eval", "sr_fitness", "sr_sse", "classification_accuracy", "eval_paired", "select_strategy", "workspace_size", "Workspace",
     "check_device_flags", "EvogpError", "last_launch_count", "set_kernel_timing", "STRATEGIES",
     "GPConfig", "generate", "subtree_exchange", "tournament", "reproduce", "Evolution",
 ]
@@ -73,6 +73,31 @@ def tensorize(offsets, types, values, max_len: int, n_inputs: int, n_outputs: in
     if st != OK:
         raise EvogpError(st, "evogp_tensorize", int(et[0]), int(en[0]))
     return ot, ov, osz
+
+
+def tensorize_device(offsets, types, values, max_len: int, n_inputs: int, n_outputs: int = 1, out=None,
+                     status: bool = True, stream=None):
+    """Device: prefix CSR lists (CUDA tensors: offsets int64 [P+1], types
+    int16, values float32) -> (type, value, size) [P, max_len] CUDA tensors
+    and per-tree status int32 [P] (0 or the EVOGP_E_* code), or None."""
+    import torch
+
+    P = int(offsets.numel()) - 1
+    dev = offsets.device
+    for a, dt in ((offsets, torch.int64), (types, torch.int16), (values, torch.float32)):
+        if not a.is_cuda or a.dtype != dt or not a.is_contiguous():
+            raise ValueError("offsets / types / values must be contiguous CUDA int64 / int16 / float32 tensors")
+    if out is None:
+        out = (torch.empty((P, max_len), dtype=torch.int16, device=dev),
+               torch.empty((P, max_len), dtype=torch.float32, device=dev),
+               torch.empty((P, max_len), dtype=torch.int16, device=dev))
+    st = torch.empty(P, dtype=torch.int32, device=dev) if status else None
+    t, v, s = out
+    rc = _LIB.evogp_tensorize_device(P, _vp(offsets), _vp(types), _vp(values), max_len, n_inputs, n_outputs, _vp(t),
+                                     _vp(v), _vp(s), _vp(st), _stream_ptr(stream, dev))
+    if rc != OK:
+        raise EvogpError(rc, "evogp_tensorize_device")
+    return t, v, s, st
 
 
 def workspace_size(P: int, D: int, max_len: int, n_inputs: int, n_outputs: int = 1) -> int:

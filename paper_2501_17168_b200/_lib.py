@@ -24,6 +24,7 @@ EXPORTS = (
     "evogp_select_strategy", "evogp_check_device_flags", "evogp_status_string", "evogp_last_error",
     "evogp_last_launch_count", "evogp_set_kernel_timing", "evogp_classification_accuracy",
     "evogp_eval_paired", "evogp_generate", "evogp_subtree_exchange", "evogp_tournament", "evogp_reproduce",
+    "evogp_tensorize_device",
 )
 
 
@@ -36,6 +37,8 @@ def load() -> ctypes.CDLL:
     i64, i32, vp, sz = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t
     lib.evogp_tensorize.argtypes = [i64, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp]
     lib.evogp_tensorize.restype = ctypes.c_int
+    lib.evogp_tensorize_device.argtypes = [i64, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp]
+    lib.evogp_tensorize_device.restype = ctypes.c_int
     lib.evogp_workspace_size.argtypes = [i64, i64, i32, i32, i32]
     lib.evogp_workspace_size.restype = sz
     dev_args = [vp, vp, vp, i64, i32, i32, vp, i64, i32, i32]
