@@ -185,6 +185,9 @@ __device__ __forceinline__ void vld_nc(const float* p, float (&v)[K]) {
 //   a fast path's valid range (the caller then re-runs the chunk cold).
 // COLD = true: same fast paths where valid, library functions elsewhere.
 // ------------------------------------------------------------------------
+// protected log (reading R3): |a| > delta ? log|a| : 0
+__device__ __forceinline__ float fn_plog(float a) { return fabsf(a) > kDelta ? logf(fabsf(a)) : 0.0f; }
+
 template <int K, bool MULTI, bool COLD>
 __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len, const float* __restrict__ xl,
                                           float* stk, float* accl, float (&tos)[K]) {
@@ -233,19 +236,9 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
     // straight into tos. MULTI: results go to r; a Modi node adds r to
     // acc[slot] and passes its rightmost child's value upward (unary: the
     // child itself), otherwise r becomes the new top.
-#define MODI_FIN(RIGHT)                        \
-  if constexpr (MULTI) {                       \
-    const uint32_t slot = (nd.x >> 8) & 0xFFu; \
-    if (slot != kNoSlot) {                     \
-      float* acc = accl + slot * SLOT;         \
-      float av[K];                             \
-      vld<K>(acc, av);                         \
-      FOR_K av[k] = __fadd_rn(av[k], r[k]);    \
-      vst<K>(acc, av);                         \
-      FOR_K tos[k] = RIGHT[k];                 \
-    } else {                                   \
-      FOR_K tos[k] = r[k];                     \
-    }                                          \
+#define MODI_FIN(RIGHT) \
+  if constexpr (MULTI) {  \
+    FOR_K rt[k] = RIGHT[k]; \
   }
 #define RES(k) (MULTI ? r[k] : tos[k])
 #define POP(v)   \
@@ -275,33 +268,29 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
   }
 #define BIN(F, EXPR)                     \
   case OP_FN + F: {                      \
-    float b[K], r[K];                    \
+    float b[K];                          \
     POPB(b)                              \
     FOR_K {                              \
       const float a = tos[k], bb = b[k]; \
       RES(k) = (EXPR);                   \
     }                                    \
     MODI_FIN(b)                          \
-    (void)r;                             \
     break;                               \
   }
 #define UN(F, EXPR)           \
   case OP_FN + F: {           \
     UNPRE                     \
-    float r[K];               \
     FOR_K {                   \
       const float a = tos[k]; \
       RES(k) = (EXPR);        \
     }                         \
     MODI_FIN(tos)             \
-    (void)r;                  \
     break;                    \
   }
 // range-checked unary: one check per node (max |x| over the K points)
 #define UN_RANGED(F, OK_MAX, FAST, SLOW_EXPR)                    \
   case OP_FN + F: {                                              \
     UNPRE                                                        \
-    float r[K];                                                  \
     float m = 0.0f;                                              \
     FOR_K m = fmaxf(m, fabsf(tos[k]));                           \
     if constexpr (COLD) {                                        \
@@ -314,10 +303,12 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
       FOR_K RES(k) = FAST(tos[k]);                               \
     }                                                            \
     MODI_FIN(tos)                                                \
-    (void)r;                                                     \
     (void)m;                                                     \
     break;                                                       \
   }
+    float r[K], rt[K];  // MULTI: the node's result and its rightmost child's value
+    (void)r;
+    (void)rt;
     switch (op) {
       BIN(F_ADD, __fadd_rn(a, bb))
       BIN(F_SUB, __fsub_rn(a, bb))
@@ -327,7 +318,7 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
 // K points; the rare small min is re-checked exactly).
 #define DIV_CASE(OPC, NUM, DEN)                                                     \
   case OPC: {                                                                       \
-    float b[K], r[K];                                                               \
+    float b[K];                                                                     \
     POPB(b)                                                                         \
     float mx = 0.0f, mn = kDivRange;                                                \
     FOR_K {                                                                         \
@@ -349,7 +340,6 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
       FOR_K RES(k) = fabsf(DEN[k]) > kDelta ? div_fast(NUM[k], DEN[k]) : 1.0f;      \
     }                                                                               \
     MODI_FIN(b)                                                                     \
-    (void)r;                                                                        \
     break;                                                                          \
   }
       DIV_CASE(OP_FN + F_DIV, tos, b)
@@ -363,7 +353,7 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
 // register rotation (static indices, no K-fold code duplication)
 #define POW_CASE(OPC, BASE, EXPO)          \
   case OPC: {                              \
-    float b[K], r[K], a[K], e[K];          \
+    float b[K], a[K], e[K];                \
     POPB(b)                                \
     FOR_K {                                \
       a[k] = BASE[k];                      \
@@ -381,20 +371,41 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
     }                                      \
     FOR_K RES(k) = a[k];                   \
     MODI_FIN(b)                            \
-    (void)r;                               \
     break;                                 \
   }
       POW_CASE(OP_FN + F_POW, tos, b)
       POW_CASE(OP_FN + F_POW_R, b, tos)
       BIN(F_SUB_R, __fsub_rn(bb, a))
-      UN(F_LOG, fabsf(a) > kDelta ? logf(fabsf(a)) : 0.0f)
-      UN(F_EXP, expf(a))
-      UN(F_TANH, tanhf(a))
+// libm-bodied unary functions. Multi-output programs apply one inlined body
+// to the K points by register rotation (static indices, no K-fold code
+// duplication): their kernel's hot code otherwise overflows the instruction
+// cache (ncu: 'no instruction' the top stall on c5). Single-output programs
+// keep the K unrolled bodies (the rotation costs them registers).
+#define UN_ROT(F, FN)                                                        \
+  case OP_FN + F: {                                                          \
+    UNPRE                                                                    \
+    if constexpr (MULTI) {                                                   \
+      float a[K];                                                            \
+      FOR_K a[k] = tos[k];                                                   \
+      _Pragma("unroll 1") for (int it = 0; it < K; ++it) {                   \
+        const float v = FN(a[0]);                                            \
+        _Pragma("unroll") for (int k = 0; k < K - 1; ++k) a[k] = a[k + 1];   \
+        a[K - 1] = v;                                                        \
+      }                                                                      \
+      FOR_K RES(k) = a[k];                                                   \
+    } else {                                                                 \
+      FOR_K RES(k) = FN(tos[k]);                                             \
+    }                                                                        \
+    MODI_FIN(tos)                                                            \
+    break;                                                                   \
+  }
+      UN_ROT(F_LOG, fn_plog)
+      UN_ROT(F_EXP, expf)
+      UN_ROT(F_TANH, tanhf)
       UN(F_NEG, -a)
       UN(F_ABS, fabsf(a))
       case OP_FN + F_SQRT: {  // sqrt(|a|)
         UNPRE
-        float r[K];
         float mx = 0.0f;
         uint32_t mn = 0xFFFFFFFFu;  // zero excluded, as in DIV
         FOR_K {
@@ -415,12 +426,10 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
           }
         }
         MODI_FIN(tos)
-        (void)r;
         break;
       }
       case OP_FN + F_INV: {  // |a| > delta ? 1 / a : 0
         UNPRE
-        float r[K];
         float mx = 0.0f;
         FOR_K mx = fmaxf(mx, fabsf(tos[k]));
         if constexpr (COLD) {
@@ -433,7 +442,6 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
           FOR_K RES(k) = fabsf(tos[k]) > kDelta ? rcp_fast(tos[k]) : 0.0f;
         }
         MODI_FIN(tos)
-        (void)r;
         break;
       }
       BIN(F_LT, a < bb ? 1.0f : 0.0f)
@@ -441,13 +449,28 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
       BIN(F_LE, a <= bb ? 1.0f : 0.0f)
       BIN(F_GE, a >= bb ? 1.0f : 0.0f)
       default: {  // F_IF (ternary): a = tos, b = first pop, c = second pop
-        float b[K], c[K], r[K];
+        float b[K], c[K];
         POP(b);
         POP(c);
         FOR_K RES(k) = tos[k] > 0.0f ? b[k] : c[k];
         MODI_FIN(c)
-        (void)r;
         break;
+      }
+    }
+    // MULTI (PAPER §IV-C, reading R4): a Modi node adds its value
+    // to out[slot] and passes its rightmost child's value upward; any other
+    // node's value becomes the new top. One shared copy for every case.
+    if constexpr (MULTI) {
+      const uint32_t slot = (nd.x >> 8) & 0xFFu;
+      if (slot != kNoSlot) {
+        float* acc = accl + slot * SLOT;
+        float av[K];
+        vld<K>(acc, av);
+        FOR_K av[k] = __fadd_rn(av[k], r[k]);
+        vst<K>(acc, av);
+        FOR_K tos[k] = rt[k];
+      } else {
+        FOR_K tos[k] = r[k];
       }
     }
 #undef RES
@@ -461,6 +484,7 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
 #undef MODI_FIN
 #undef DIV_CASE
 #undef POW_CASE
+#undef UN_ROT
     if (!COLD && bail) break;  // this lane's result is discarded; stop early
   }
   return bail;
