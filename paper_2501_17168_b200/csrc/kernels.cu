@@ -1457,10 +1457,21 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   const int depth = max_depth_bound(L);
   const int prog_ld = static_cast<int>(round_up(L + 1, 2));  // node words per program row (16-byte rows)
   const int tree_bytes = prog_ld * 8;
-  // shared-memory budget: aim at `target_warps` resident warps per SM
-  const int budget_per_warp = (227 * 1024) / target_warps;
-  const int per_warp_fixed = acc_bytes + (strategy == EVOGP_STRATEGY_INTER ? tree_bytes : 0);
-  int SD = (budget_per_warp - per_warp_fixed) / slot_bytes;
+  // shared-memory budget: aim at `target_warps` resident warps per SM.
+  // (a): 227 KB / target per warp (measured best, profiles/sweep_kw_r01.txt;
+  // sizing by CTA instead — 4 more warps on c4 / c5 / g1 at one slot less —
+  // measured +4% on c4's kernel but -16% on c5 and -3% on g1).
+  // (b): per 8-warp CTA, the CTAs holding `target_warps` warps must fit the
+  // SM's 228 KB with the 1 KB the runtime reserves per CTA (per-warp sizing
+  // rounded c3 down to 3 CTAs = 24 warps; this gives 4 CTAs: +11% on c3)
+  int SD;
+  if (strategy == EVOGP_STRATEGY_INTER) {
+    SD = ((227 * 1024) / target_warps - acc_bytes - tree_bytes) / slot_bytes;
+  } else {
+    const int ctas = std::max(1, target_warps / warps);
+    const int cta_budget = (228 * 1024) / ctas - 1024 - 128;  // + static shared memory margin
+    SD = ((cta_budget - tree_bytes) / warps - acc_bytes) / slot_bytes;
+  }
   SD = std::max(2, std::min(SD, std::max(1, depth - 1)));
   const int warp_smem = acc_bytes + SD * slot_bytes;
   const size_t smem = strategy == EVOGP_STRATEGY_INTER
