@@ -190,7 +190,9 @@ __device__ __forceinline__ float fn_plog(float a) { return fabsf(a) > kDelta ? l
 
 template <int K, bool MULTI, bool COLD>
 __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len, const float* __restrict__ xl,
-                                          float* stk, float* accl, float (&tos)[K]) {
+                                          float* stk, float* accl, float (&tos)[K], int aslot = 32 * K) {
+  // aslot: float stride between the Modi accumulators of two output slots
+  // (32 K, or the enclosing K-point layout's stride in a multi-pass run)
   constexpr int SLOT = 32 * K;
   float* top = stk;
   bool bail = false;
@@ -463,7 +465,7 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
     if constexpr (MULTI) {
       const uint32_t slot = (nd.x >> 8) & 0xFFu;
       if (slot != kNoSlot) {
-        float* acc = accl + slot * SLOT;
+        float* acc = accl + slot * aslot;
         float av[K];
         vld<K>(acc, av);
         FOR_K av[k] = __fadd_rn(av[k], r[k]);
@@ -528,20 +530,31 @@ __device__ __forceinline__ void zero_acc(float* s_acc_l, int n_out) {
 // slice of the K layout [K/4 groups][32 lanes][4] starting at point H*q of
 // every lane (H divides 4), so pass q yields tos[H*q .. H*q+H-1] — the same
 // values, in the same order of operations, as a single K-point run.
-template <int K, int H>
+template <int K, int H, bool MULTI>
 __device__ __forceinline__ void run_passes(const Node* tree, int len, const float* xl, int lane, float* s_stack_l,
-                                           float* s_acc_l, float (&tos)[K], unsigned* cold) {
+                                           float* s_acc_l, float (&tos)[K], unsigned* cold, int n_out) {
   constexpr int NP = K / H;
   static_assert(H >= 1 && K % H == 0 && (H >= 4 || 4 % H == 0), "pass width");
   float* stk = s_stack_l - lane * Lay<K>::V + lane * Lay<H>::V;
 #pragma unroll 1
   for (int q = 0; q < NP; ++q) {
-    const float* xq = xl + (H * q / 4) * 128 + (H * q) % 4;
+    const int off = (H * q / 4) * 128 + (H * q) % 4;
+    const float* xq = xl + off;
+    // multi-output: the pass's slice of the K-point Modi accumulators (same
+    // offsets as its datapoints; slots 32 K floats apart)
+    float* accq = s_acc_l + off;
     float th[H];
-    const bool bail = interpret<H, false, false>(tree, len, xq, stk, s_acc_l, th);
+    const bool bail = interpret<H, MULTI, false>(tree, len, xq, stk, accq, th, 32 * K);
     if (__any_sync(FULL_MASK, bail)) {
       if (lane == 0) atomicAdd(cold, 1u);
-      interpret<H, false, true>(tree, len, xq, stk, s_acc_l, th);
+      if (MULTI) {
+        __syncwarp();
+        float z[H];
+#pragma unroll
+        for (int k = 0; k < H; ++k) z[k] = 0.f;
+        for (int o = 0; o < n_out; ++o) vst<H>(accq + o * (32 * K), z);
+      }
+      interpret<H, MULTI, true>(tree, len, xq, stk, accq, th, 32 * K);
     }
 #pragma unroll
     for (int k = 0; k < K; ++k)
@@ -573,20 +586,20 @@ __device__ __forceinline__ void run_chunk(const KParams& p, const Node* tree, co
     }
     return;
   }
-  if constexpr (!MULTI && K >= 2) {
+  if constexpr (K >= 2) {
     if (need <= 2 * p.SD) {
-      run_passes<K, K / 2>(tree, ti.len, xl, lane, s_stack_l, s_acc_l, tos, &p.ctl->cold_chunks);
+      run_passes<K, K / 2, MULTI>(tree, ti.len, xl, lane, s_stack_l, s_acc_l, tos, &p.ctl->cold_chunks, p.n_out);
       return;
     }
     if constexpr (K >= 4) {
       if (need <= 4 * p.SD) {
-        run_passes<K, K / 4>(tree, ti.len, xl, lane, s_stack_l, s_acc_l, tos, &p.ctl->cold_chunks);
+        run_passes<K, K / 4, MULTI>(tree, ti.len, xl, lane, s_stack_l, s_acc_l, tos, &p.ctl->cold_chunks, p.n_out);
         return;
       }
     }
     if constexpr (K >= 8) {
       if (need <= 8 * p.SD) {
-        run_passes<K, K / 8>(tree, ti.len, xl, lane, s_stack_l, s_acc_l, tos, &p.ctl->cold_chunks);
+        run_passes<K, K / 8, MULTI>(tree, ti.len, xl, lane, s_stack_l, s_acc_l, tos, &p.ctl->cold_chunks, p.n_out);
         return;
       }
     }

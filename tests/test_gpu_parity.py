@@ -750,3 +750,29 @@ def test_inconsistent_sizes_skip_reordering():
         for strategy in ("inter", "intra"):
             g = gpu_eval(dev, X, 1, strategy)[:, :, 0]
             assert same_bits_mod_zero(g, r32).all(), strategy
+
+
+def test_multi_output_deep_rows_multipass():
+    """Modi programs are never reordered, so deep multi-output rows run the
+    2/4/8-pass split with per-pass slices of the Modi accumulators (or the
+    global stacks): outputs bit-exact vs the FP32-faithful oracle, and the
+    fused classification accuracy equal to the oracle's on those outputs."""
+    evogp = _evogp()
+    L, n_in, n_out, D = 255, 3, 6, 300
+    cfg = dict(max_len=L, n_inputs=n_in, n_outputs=n_out, funcs=list(synth.M_IEEE), const_lo=-1.0, const_hi=1.0,
+               p_const=0.5, p_leaf=0.02, p_modi=0.3, depth_min=6, depth_max=14, tournament_size=2,
+               p_crossover=0.0, p_mutation=0.0, crossover_kind=0, leaf_bias=0.1, mutation_weights=[1] + [0] * 7,
+               point_rate=0.1, const_sigma=0.1, subtree_depth=4)
+    t, v, s = oracle.generate(240, cfg, 77)
+    X = synth.dataset_X(14, 0, D, n_in, lo=0.5, hi=1.5)
+    r32 = oracle.evaluate(t, v, s, X, n_out=n_out, mode=1)
+    labels = (np.arange(D) % n_out).astype(np.int32)
+    acc_ref = oracle.accuracy(r32.astype(np.float32).astype(np.float64), labels)
+    dev = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (t, v, s)]
+    Xd = torch.from_numpy(X).cuda()
+    ld = torch.from_numpy(labels).cuda()
+    for strategy in ("inter", "intra"):
+        g = gpu_eval(dev, X, n_out, strategy)
+        assert same_bits_mod_zero(g, r32).all(), strategy
+        acc = evogp.classification_accuracy(*dev, Xd, ld, n_out, strategy=strategy).cpu().numpy()
+        assert np.array_equal(acc, acc_ref), strategy
