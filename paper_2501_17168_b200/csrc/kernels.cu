@@ -918,25 +918,18 @@ __device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __res
         }
       }
     }
+    // branch-free iterations (selects only: no divergence bookkeeping)
     uint8_t swp = 0;
     while (!__all_sync(FULL_MASK, q != 0)) {
       const int x1 = __shfl_sync(FULL_MASK, q, l1);
       const int x2 = __shfl_sync(FULL_MASK, q, l2);
       const int x3 = __shfl_sync(FULL_MASK, q, l3);
-      if (q == 0) {
-        const int n1 = v1 ? v1 : x1, n2 = v2 ? v2 : x2, n3 = v3 ? v3 : x3;
-        if (n1 && n2 && n3) {
-          if (ar == 1) {
-            q = n1;
-          } else if (ar == 2) {
-            const int q_def = max(n2, n1 + 1), q_swp = max(n1, n2 + 1);
-            swp = q_swp < q_def;
-            q = min(q_def, q_swp);
-          } else {
-            q = max(n3, max(n2 + 1, n1 + 2));
-          }
-        }
-      }
+      const int n1 = v1 ? v1 : x1, n2 = v2 ? v2 : x2, n3 = v3 ? v3 : x3;
+      const int q_def = max(n2, n1 + 1), q_swp = max(n1, n2 + 1);
+      const int q_new = ar == 1 ? n1 : (ar == 2 ? min(q_def, q_swp) : max(n3, max(n2 + 1, n1 + 2)));
+      const bool now = q == 0 && n1 != 0 && n2 != 0 && n3 != 0;
+      swp = (now && ar == 2) ? static_cast<uint8_t>(q_swp < q_def) : swp;
+      q = now ? q_new : q;
     }
     if (i < n) {
       nd[i] = static_cast<uint16_t>(q);
