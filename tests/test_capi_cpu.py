@@ -131,3 +131,31 @@ def test_workspace_and_selector_host():
     # small D -> hybrid (inter), large D -> data-level (intra)
     assert evogp.select_strategy(10_000, 1024, 63) == "inter"
     assert evogp.select_strategy(1000, 1 << 20, 127) == "intra"
+
+
+def test_gp_config_struct_layout_matches_header(tmp_path):
+    """The ctypes mirror of evogp_gp_config (paper_2501_17168_b200/gp.py) has
+    the C header's size and field offsets (compiled with gcc from include/)."""
+    from paper_2501_17168_b200.gp import _CCfg
+
+    fields = [f for f, _ in _CCfg._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text("#include <stdio.h>\n#include <stddef.h>\n#include \"evogp.h\"\nint main(void){\n"
+                   "printf(\"%zu\\n\", sizeof(evogp_gp_config));\n" +
+                   "".join(f"printf(\"%zu\\n\", offsetof(evogp_gp_config, {f}));\n" for f in fields) +
+                   "return 0;}\n")
+    exe = tmp_path / "layout"
+    import subprocess
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    out = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    assert out[0] == ctypes.sizeof(_CCfg)
+    assert out[1:] == [getattr(_CCfg, f).offset for f in fields]
+
+
+def test_gp_config_defaults_follow_tab_sr_params():
+    """tab:sr_params: tournament 20, p_c 0.9, p_m 0.1, max size 512, {+,-,x,/,sin,cos,tan}."""
+    from paper_2501_17168_b200.gp import GPConfig
+
+    c = GPConfig()
+    assert (c.tournament_size, c.p_crossover, c.p_mutation, c.max_len) == (20, 0.9, 0.1, 512)
+    assert c.c().func_mask == sum(1 << f for f in (0, 1, 2, 3, 4, 5, 6))
