@@ -44,7 +44,11 @@ struct TreeInfo {
   int len;
   int maxdepth;
   bool valid;
+  bool paper = false;  // every function is one of the paper's set {+,-,*,/,sin,cos,tan}
 };
+
+// TreeMeta.maxdepth bit 30 flags a paper-set row (valid rows only)
+constexpr int32_t kPaperRow = 1 << 30;
 
 // One warp decodes row `tp` into Node words: node i goes to s_tree[i + 1]
 // (s_tree[0] is a pad). Validation: with c_i = 1 - arity_i the stack size
@@ -58,6 +62,7 @@ __device__ __forceinline__ TreeInfo stage_tree_warp(const KParams& p, int64_t tp
   const int len = min(max(len0, 1), p.L);
   bool ok = len0 >= 1 && len0 <= p.L;
   int carry = 0, mind = INT_MAX, maxd = 0;
+  bool paper = true;
   const int nblk = (len + 31) >> 5;
   for (int b = nblk - 1; b >= 0; --b) {
     const int i = b * 32 + lane;
@@ -70,6 +75,7 @@ __device__ __forceinline__ TreeInfo stage_tree_warp(const KParams& p, int64_t tp
       ok = decode_node(t, v, p.n_in, p.n_out, p.Dpad, nd, ar) && ok;
       s_tree[i + 1] = nd;
       c = 1 - ar;
+      paper = paper && (nd.w0 & 0xFFu) <= OP_FN + F_TAN;
     }
     int s = c;  // inclusive suffix scan over lanes lane..31
 #pragma unroll
@@ -96,6 +102,7 @@ __device__ __forceinline__ TreeInfo stage_tree_warp(const KParams& p, int64_t tp
   ti.len = len;
   ti.maxdepth = maxd;
   ti.valid = ok && mind >= 1 && carry == 1;
+  ti.paper = __all_sync(FULL_MASK, paper);
   return ti;
 }
 
@@ -188,7 +195,7 @@ __device__ __forceinline__ void vld_nc(const float* p, float (&v)[K]) {
 // protected log (reading R3): |a| > delta ? log|a| : 0
 __device__ __forceinline__ float fn_plog(float a) { return fabsf(a) > kDelta ? logf(fabsf(a)) : 0.0f; }
 
-template <int K, bool MULTI, bool COLD>
+template <int K, bool MULTI, bool COLD, bool PAPER = false>
 __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len, const float* __restrict__ xl,
                                           float* stk, float* accl, float (&tos)[K], int aslot = 32 * K) {
   // aslot: float stride between the Modi accumulators of two output slots
@@ -311,6 +318,7 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
     float r[K], rt[K];  // MULTI: the node's result and its rightmost child's value
     (void)r;
     (void)rt;
+    if constexpr (!PAPER) {
     switch (op) {
       BIN(F_ADD, __fadd_rn(a, bb))
       BIN(F_SUB, __fsub_rn(a, bb))
@@ -459,6 +467,27 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
         break;
       }
     }
+    } else {
+      // rows whose functions are all in the paper's set: the same
+      // cases (same arithmetic) behind a 9-way dispatch instead of a 26-way
+      // one, and a much smaller hot loop for the instruction caches. Any
+      // other op (impossible for a row flagged by the compile pass) bails to
+      // the full cold copy.
+      switch (op) {
+        BIN(F_ADD, __fadd_rn(a, bb))
+        BIN(F_SUB, __fsub_rn(a, bb))
+        BIN(F_MUL, __fmul_rn(a, bb))
+        DIV_CASE(OP_FN + F_DIV, tos, b)
+        DIV_CASE(OP_FN + F_DIV_R, b, tos)
+        UN_RANGED(F_SIN, kTrigReduceMax, fm_sin_fast, slow_sinf(a))
+        UN_RANGED(F_COS, kTrigReduceMax, fm_cos_fast, slow_cosf(a))
+        UN_RANGED(F_TAN, kTrigReduceMax, fm_tan_fast, slow_tanf(a))
+        BIN(F_SUB_R, __fsub_rn(bb, a))
+        default:
+          bail = true;
+          break;
+      }
+    }
     // MULTI (PAPER §IV-C, reading R4): a Modi node adds its value
     // to out[slot] and passes its rightmost child's value upward; any other
     // node's value becomes the new top. One shared copy for every case.
@@ -575,7 +604,8 @@ __device__ __forceinline__ void run_chunk(const KParams& p, const Node* tree, co
   if (MULTI) zero_acc<K>(s_acc_l, p.n_out);
   const int need = ti.maxdepth - 1;  // stack slots below the register top
   if (need <= p.SD) {
-    const bool bail = interpret<K, MULTI, false>(tree, ti.len, xl, s_stack_l, s_acc_l, tos);
+    const bool bail = ti.paper ? interpret<K, MULTI, false, true>(tree, ti.len, xl, s_stack_l, s_acc_l, tos)
+                               : interpret<K, MULTI, false>(tree, ti.len, xl, s_stack_l, s_acc_l, tos);
     if (__any_sync(FULL_MASK, bail)) {
       if (lane == 0) atomicAdd(&p.ctl->cold_chunks, 1u);
       if (MULTI) {
@@ -1139,7 +1169,7 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
     }
   compiled:
     if (lane == 0) {
-      p.info[tp] = TreeMeta{ti.len, ti.valid ? ti.maxdepth : -1};
+      p.info[tp] = TreeMeta{ti.len, ti.valid ? (ti.maxdepth | (ti.paper ? kPaperRow : 0)) : -1};
       if (!ti.valid) atomicOr(&p.ctl->flags, 1);
     }
     __syncwarp();
@@ -1153,7 +1183,7 @@ __device__ __forceinline__ TreeInfo load_program_warp(const KParams& p, int64_t 
   uint2* dst = reinterpret_cast<uint2*>(s_tree);
   for (int i = lane; i <= m.len; i += 32) dst[i] = src[i];
   __syncwarp();
-  return TreeInfo{m.len, m.maxdepth, m.maxdepth >= 0};
+  return TreeInfo{m.len, m.maxdepth & (kPaperRow - 1), m.maxdepth >= 0, m.maxdepth >= 0 && (m.maxdepth & kPaperRow)};
 }
 
 // ------------------------------------------------------------------------
@@ -1261,7 +1291,8 @@ __global__ void __launch_bounds__(32 * kIntraWarps) k_intra(const KParams p) {
           "l"(p.prog + tp * p.prog_ld), "r"(row_bytes), "r"(bar)
           : "memory");
       const TreeMeta m = p.info[tp];
-      s_info = TreeInfo{m.len, m.maxdepth, m.maxdepth >= 0};
+      s_info = TreeInfo{m.len, m.maxdepth & (kPaperRow - 1), m.maxdepth >= 0,
+                        m.maxdepth >= 0 && (m.maxdepth & kPaperRow)};
       uint32_t done = 0;
       while (!done) {
         asm volatile(
