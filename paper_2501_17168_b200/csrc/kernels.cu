@@ -1198,7 +1198,7 @@ __device__ __forceinline__ long long next_ticket(const KParams& p, int lane) {
 }
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(32 * kInterWarps) k_inter(const KParams p) {
+__global__ void __launch_bounds__(32 * kInterWarps, 8) k_inter(const KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int V = Lay<K>::V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
