@@ -1248,7 +1248,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
 }
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(32 * kIntraWarps) k_intra(const KParams p) {
+__global__ void __launch_bounds__(32 * kIntraWarps, 4) k_intra(const KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ double s_red[kIntraWarps];
