@@ -1,0 +1,91 @@
+"""Streaming SR fitness from host prefix lists (the end-to-end public path).
+
+A population held on the host as prefix lists (CSR: offsets int64 [P+1],
+types int16, values float32, in pinned memory) is scored chunk by chunk on
+two CUDA streams, so the host->device copy of chunk c+1 overlaps the
+device tensorize (evogp_tensorize_device, row a1) and the fused SR fitness
+(evogp_sr_fitness, rows a2-a7) of chunk c; each chunk's MSEs go back to the
+host as soon as they are ready. Argument marshalling and stream plumbing
+only: every step runs in libevogp.so's kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+
+from ._lib import OK
+
+
+class HostSRFitness:
+    """Reusable pipeline for populations of up to `P_max` trees / `nodes_max`
+    nodes over a fixed dataset (X row-major D x n_inputs, y), on one device."""
+
+    def __init__(self, P_max: int, nodes_max: int, max_len: int, n_inputs: int, X, y, chunks: int = 4,
+                 device=None, strategy="auto"):
+        import torch
+
+        from . import Workspace
+
+        self.dev = torch.device(device) if device is not None else X.device
+        self.L, self.n_in, self.strategy = max_len, n_inputs, strategy
+        self.chunks = max(1, int(chunks))
+        self.X, self.y = X, y
+        pc = (P_max + self.chunks - 1) // self.chunks
+        self.pc = pc
+        mk = lambda *shape, dt: torch.empty(shape, dtype=dt, device=self.dev)  # noqa: E731
+        # double buffers: chunk c uses set c % 2
+        self.d_off = [mk(pc + 1, dt=torch.int64) for _ in range(2)]
+        self.d_ty = [mk(nodes_max, dt=torch.int16) for _ in range(2)]
+        self.d_va = [mk(nodes_max, dt=torch.float32) for _ in range(2)]
+        self.rows = [(mk(pc, max_len, dt=torch.int16), mk(pc, max_len, dt=torch.float32),
+                      mk(pc, max_len, dt=torch.int16)) for _ in range(2)]
+        self.mse = [mk(pc, dt=torch.float64) for _ in range(2)]
+        self.ws = [Workspace(pc, int(X.shape[0]), max_len, n_inputs, 1, device=self.dev) for _ in range(2)]
+        self.s_copy = torch.cuda.Stream(device=self.dev)
+        self.s_comp = torch.cuda.Stream(device=self.dev)
+        self.ev_h2d = [torch.cuda.Event() for _ in range(2)]
+        self.ev_free = [torch.cuda.Event() for _ in range(2)]
+        for e in self.ev_free:
+            e.record(self.s_comp)
+
+    def __call__(self, offsets, types, values, out):
+        """offsets/types/values: pinned host torch tensors (CSR); out: pinned
+        host float64 tensor [P]. Returns out (after synchronising)."""
+        import torch
+
+        from . import _LIB, EvogpError, sr_fitness
+
+        P = int(offsets.numel()) - 1
+        off_np = offsets.numpy()
+        bounds = [min(P, c * self.pc) for c in range(self.chunks + 1)]
+        for c in range(self.chunks):
+            p0, p1 = bounds[c], bounds[c + 1]
+            if p1 <= p0:
+                continue
+            b = c & 1
+            n0, n1 = int(off_np[p0]), int(off_np[p1])
+            with torch.cuda.stream(self.s_copy):
+                self.s_copy.wait_event(self.ev_free[b])
+                self.d_off[b][: p1 - p0 + 1].copy_(offsets[p0: p1 + 1], non_blocking=True)
+                self.d_ty[b][: n1 - n0].copy_(types[n0:n1], non_blocking=True)
+                self.d_va[b][: n1 - n0].copy_(values[n0:n1], non_blocking=True)
+                self.ev_h2d[b].record(self.s_copy)
+            with torch.cuda.stream(self.s_comp):
+                self.s_comp.wait_event(self.ev_h2d[b])
+                t, v, s = (r[: p1 - p0] for r in self.rows[b])
+                # the chunk's offsets are global node indices: pass node arrays
+                # based n0 elements before the copied slice (never dereferenced there)
+                st = _LIB.evogp_tensorize_device(
+                    p1 - p0, ctypes.c_void_p(self.d_off[b].data_ptr()),
+                    ctypes.c_void_p(self.d_ty[b].data_ptr() - 2 * n0),
+                    ctypes.c_void_p(self.d_va[b].data_ptr() - 4 * n0), self.L, self.n_in, 1,
+                    ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(s.data_ptr()),
+                    ctypes.c_void_p(0), ctypes.c_void_p(self.s_comp.cuda_stream))
+                if st != OK:
+                    raise EvogpError(st, "evogp_tensorize_device")
+                m = self.mse[b][: p1 - p0]
+                sr_fitness(t, v, s, self.X, self.y, strategy=self.strategy, out=m, workspace=self.ws[b],
+                           stream=self.s_comp)
+                out[p0:p1].copy_(m, non_blocking=True)
+                self.ev_free[b].record(self.s_comp)
+        self.s_comp.synchronize()
+        return out

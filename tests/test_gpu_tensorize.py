@@ -80,3 +80,27 @@ def test_tensorize_device_rows_evaluate():
     m1 = e.sr_fitness(t, v, s, Xd, yd).cpu().numpy()
     m2 = e.sr_fitness(*h, Xd, yd).cpu().numpy()
     assert (m1.view(np.uint64) == m2.view(np.uint64)).all()
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 4])
+def test_host_streaming_sr_fitness_matches_one_pass(chunks):
+    """The streaming public path (HostSRFitness: chunked H2D overlapped with
+    device tensorize + fused fitness) returns exactly the one-pass MSEs."""
+    e = _e()
+    from paper_2501_17168_b200.stream import HostSRFitness
+
+    cfg = synth.CONFIGS["c4"]
+    P = 30001
+    pt = synth.trees(cfg.seed, 0, P, cfg.max_len, synth.M_PAPER, cfg.n_in)
+    X, y = synth.config_data(cfg)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    h = [torch.from_numpy(a).cuda() for a in e.tensorize(pt.offsets, pt.types, pt.values, cfg.max_len, cfg.n_in)]
+    ref = e.sr_fitness(*h, Xd, yd).cpu().numpy()
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    h_off, h_ty, h_va = pin(pt.offsets.astype(np.int64)), pin(pt.types), pin(pt.values)
+    out = torch.empty(P, dtype=torch.float64).pin_memory()
+    pipe = HostSRFitness(P, int(h_ty.numel()), cfg.max_len, cfg.n_in, Xd, yd, chunks=chunks)
+    for _ in range(2):  # reuse across calls
+        out.fill_(-1.0)
+        got = pipe(h_off, h_ty, h_va, out).numpy()
+        assert (got.view(np.uint64) == ref.view(np.uint64)).all()
