@@ -516,7 +516,9 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
 #undef DIV_CASE
 #undef POW_CASE
 #undef UN_ROT
-    if (!COLD && bail) break;  // this lane's result is discarded; stop early
+    // (no per-lane early exit on bail: a divergent break costs BREAK/PLOP3
+    // bookkeeping on every node, and bailing chunks are rare — the warp
+    // finishes and re-runs the chunk on the cold copy)
   }
   return bail;
 }
