@@ -296,8 +296,10 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
     MODI_FIN(tos)             \
     break;                    \
   }
-// range-checked unary: one check per node (max |x| over the K points)
-#define UN_RANGED(F, OK_MAX, FAST, SLOW_EXPR)                    \
+// range-checked unary: one check per node (max |x| over the K points); in
+// the hot copy a warp whose points are all within SMALL_MAX takes the
+// reduction-free SMALL form (bit-identical there, fastmath.cuh)
+#define UN_RANGED(F, OK_MAX, FAST, SLOW_EXPR, SMALL_MAX, SMALL)   \
   case OP_FN + F: {                                              \
     UNPRE                                                        \
     float m = 0.0f;                                              \
@@ -309,7 +311,11 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
       }                                                          \
     } else {                                                     \
       bail |= !(m <= OK_MAX);                                    \
-      FOR_K RES(k) = FAST(tos[k]);                               \
+      if (__all_sync(FULL_MASK, m <= SMALL_MAX)) {               \
+        FOR_K RES(k) = SMALL(tos[k]);                            \
+      } else {                                                   \
+        FOR_K RES(k) = FAST(tos[k]);                             \
+      }                                                          \
     }                                                            \
     MODI_FIN(tos)                                                \
     (void)m;                                                     \
@@ -354,9 +360,9 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
   }
       DIV_CASE(OP_FN + F_DIV, tos, b)
       DIV_CASE(OP_FN + F_DIV_R, b, tos)  // children swapped by the compile pass
-      UN_RANGED(F_SIN, kTrigReduceMax, fm_sin_fast, slow_sinf(a))
-      UN_RANGED(F_COS, kTrigReduceMax, fm_cos_fast, slow_cosf(a))
-      UN_RANGED(F_TAN, kTrigReduceMax, fm_tan_fast, slow_tanf(a))
+      UN_RANGED(F_SIN, kTrigReduceMax, fm_sin_fast, slow_sinf(a), kSinCosSmall, fm_sin_small)
+      UN_RANGED(F_COS, kTrigReduceMax, fm_cos_fast, slow_cosf(a), kSinCosSmall, fm_cos_small)
+      UN_RANGED(F_TAN, kTrigReduceMax, fm_tan_fast, slow_tanf(a), kTanSmall, fm_tan_small)
       BIN(F_MAX, fmaxf(a, bb))
       BIN(F_MIN, fminf(a, bb))
 // pow(|BASE|, EXPO): one inlined powf body applied to the K points by
@@ -479,9 +485,9 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
         BIN(F_MUL, __fmul_rn(a, bb))
         DIV_CASE(OP_FN + F_DIV, tos, b)
         DIV_CASE(OP_FN + F_DIV_R, b, tos)
-        UN_RANGED(F_SIN, kTrigReduceMax, fm_sin_fast, slow_sinf(a))
-        UN_RANGED(F_COS, kTrigReduceMax, fm_cos_fast, slow_cosf(a))
-        UN_RANGED(F_TAN, kTrigReduceMax, fm_tan_fast, slow_tanf(a))
+        UN_RANGED(F_SIN, kTrigReduceMax, fm_sin_fast, slow_sinf(a), kSinCosSmall, fm_sin_small)
+        UN_RANGED(F_COS, kTrigReduceMax, fm_cos_fast, slow_cosf(a), kSinCosSmall, fm_cos_small)
+        UN_RANGED(F_TAN, kTrigReduceMax, fm_tan_fast, slow_tanf(a), kTanSmall, fm_tan_small)
         BIN(F_SUB_R, __fsub_rn(bb, a))
         default:
           bail = true;
