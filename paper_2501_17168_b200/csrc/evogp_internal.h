@@ -37,8 +37,10 @@ enum Func : int {
 enum : int { F_SUB_R = kNumFuncs, F_DIV_R, F_POW_R };
 
 // Arity per function id; kind word = 1 + arity for function nodes.
+// (bit f of 0x1FC70 = unary: SIN, COS, TAN and LOG..INV; ids >= 22 are the
+// reversed binary opcodes)
 EVOGP_HD constexpr int func_arity(int f) {
-  return (f == F_SIN || f == F_COS || f == F_TAN || (f >= F_LOG && f <= F_INV)) ? 1 : (f == F_IF ? 3 : 2);
+  return (f < 22 && ((0x1FC70u >> f) & 1u)) ? 1 : (f == F_IF ? 3 : 2);
 }
 
 // Pre-decoded node word staged in shared memory (8 bytes, one LDS.64).

@@ -790,19 +790,19 @@ __device__ __forceinline__ void combine_partial(const KParams& p, int64_t tp, in
 // Returns the program's new maximum stack depth.
 // ------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t reversed_op(uint32_t op) {
-  switch (op) {
-    case OP_FN + F_SUB: return OP_FN + F_SUB_R;
-    case OP_FN + F_DIV: return OP_FN + F_DIV_R;
-    case OP_FN + F_POW: return OP_FN + F_POW_R;
-    case OP_FN + F_SUB_R: return OP_FN + F_SUB;
-    case OP_FN + F_DIV_R: return OP_FN + F_DIV;
-    case OP_FN + F_POW_R: return OP_FN + F_POW;
-    case OP_FN + F_LT: return OP_FN + F_GT;
-    case OP_FN + F_GT: return OP_FN + F_LT;
-    case OP_FN + F_LE: return OP_FN + F_GE;
-    case OP_FN + F_GE: return OP_FN + F_LE;
-    default: return op;  // ADD, MUL, MAX, MIN are symmetric
-  }
+  // branch-free (lanes of the compile pass hold different ops): SUB <-> SUB_R,
+  // DIV <-> DIV_R, POW <-> POW_R, LT <-> GT, LE <-> GE; ADD, MUL, MAX, MIN are
+  // symmetric and keep their code
+  const uint32_t f = op - OP_FN;
+  uint32_t r = f;
+  r = f == F_SUB ? F_SUB_R : r;
+  r = f == F_SUB_R ? F_SUB : r;
+  r = f == F_DIV ? F_DIV_R : r;
+  r = f == F_DIV_R ? F_DIV : r;
+  r = f == F_POW ? F_POW_R : r;
+  r = f == F_POW_R ? F_POW : r;
+  r = (f >= F_LT && f <= F_GE) ? (((f - F_LT) ^ 1u) + F_LT) : r;
+  return OP_FN + r;
 }
 
 __device__ int reorder_program(const Node* s_nodes, int n, Node* row, unsigned char* scr, int L, int lane) {  // row: shared or global
