@@ -93,6 +93,17 @@ def main():
         s1 = unit_scale.get(res["dram__bytes_read.sum"]["unit"], 1)
         s2 = unit_scale.get(res["dram__bytes_write.sum"]["unit"], 1)
         res["dram_bytes_per_launch"] = rb * s1 + wb * s2
+    # warp-state sampling: share of samples per stall reason
+    stalls = {}
+    for i, name in enumerate(rh):
+        if name.startswith("smsp__pcsamp_warps_issue_stalled_") and not name.endswith("_not_issued"):
+            v = num(rv[i])
+            if isinstance(v, float):
+                stalls[name[len("smsp__pcsamp_warps_issue_stalled_"):]] = v
+    tot = sum(stalls.values())
+    if tot > 0:
+        res["stall_reasons_pct"] = {k: round(100.0 * v / tot, 1)
+                                    for k, v in sorted(stalls.items(), key=lambda x: -x[1])[:10]}
     # stall reasons from the source page (sampling)
     src = ncu_csv(["-i", a.report, "--page", "source", "--csv", "--print-source", "sass"])
     sh = src[1]
