@@ -1189,7 +1189,13 @@ __device__ __forceinline__ TreeInfo load_program_warp(const KParams& p, int64_t 
   const TreeMeta m = p.info[tp];
   const uint2* src = reinterpret_cast<const uint2*>(p.prog + tp * p.prog_ld);
   uint2* dst = reinterpret_cast<uint2*>(s_tree);
-  for (int i = lane; i <= m.len; i += 32) dst[i] = src[i];
+  // program rows stream through once per unit: no L1 allocation, so they do
+  // not evict the staged dataset rows the interpreter's VAR leaves read
+  for (int i = lane; i <= m.len; i += 32) {
+    uint2 w;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(w.x), "=r"(w.y) : "l"(src + i));
+    dst[i] = w;
+  }
   __syncwarp();
   return TreeInfo{m.len, m.maxdepth & (kPaperRow - 1), m.maxdepth >= 0, m.maxdepth >= 0 && (m.maxdepth & kPaperRow)};
 }
