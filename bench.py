@@ -613,12 +613,12 @@ def main():
             torch.cuda.current_stream().synchronize()
 
         e2e_mode = "one pass"
-        if cfg.n_out == 1 and axis == "pop" and world == 1 and not cfg.paired and P_local >= 100_000:
-            # large single-output populations: the streaming public path (copies of
+        n_chunks = int(os.environ.get("EVOGP_E2E_CHUNKS", "4" if P_local >= 100_000 else "1"))
+        if cfg.n_out == 1 and axis == "pop" and world == 1 and not cfg.paired and n_chunks > 1:
+            # single-output populations: the streaming public path (copies of
             # chunk c+1 overlap the device work of chunk c)
             from paper_2501_17168_b200.stream import HostSRFitness
 
-            n_chunks = 4
             pipe = HostSRFitness(P_local, int(h_ty.numel()), cfg.max_len, cfg.n_in, Xd, yd, chunks=n_chunks,
                                  strategy=strategy)
             e2e_mode = f"HostSRFitness, {n_chunks} chunks on 2 streams"
