@@ -1518,6 +1518,17 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   int SD;
   if (strategy == EVOGP_STRATEGY_INTER) {
     SD = ((227 * 1024) / target_warps - acc_bytes - tree_bytes) / slot_bytes;
+    // long rows: each warp's staged program eats the stack budget (4 KB at
+    // L = 512 leaves SD = 3 at 32 warps, and most evolved rows then run the
+    // 2-pass split). Trade resident warps for at least kMinSlots slots
+    // (measured on g1: 28 warps / SD 3 -> 2.37e12, 24 warps / SD 5 ->
+    // 3.24e12 GPops/s kernel); short rows keep the 32-warp target.
+    constexpr int kMinSlots = 5;
+    if (SD < kMinSlots && !std::getenv("EVOGP_TUNE_WARPS")) {
+      const int per_warp = acc_bytes + tree_bytes + kMinSlots * slot_bytes;
+      target_warps = std::max(16, (227 * 1024) / per_warp);
+      SD = ((227 * 1024) / target_warps - acc_bytes - tree_bytes) / slot_bytes;
+    }
   } else {
     const int ctas = std::max(1, target_warps / warps);
     const int cta_budget = (228 * 1024) / ctas - 1024 - 128;  // + static shared memory margin
