@@ -1639,9 +1639,11 @@ int launch(Plan& pl, int mode, const float* X, int32_t x_layout, const float* y,
   {
     const int64_t total = static_cast<int64_t>(kp.n_in + 1) * kp.Dpad;
     // warps per CTA such that their compile scratch fits the opt-in shared memory
+    int wpb_cap = 8;
+    if (const char* e = std::getenv("EVOGP_TUNE_PREP_WPB")) wpb_cap = std::max(1, std::min(8, std::atoi(e)));
     const int wpb = kp.reorder_scratch_bytes > 0
-                        ? std::max(1, std::min(8, (220 * 1024) / kp.reorder_scratch_bytes))
-                        : 8;
+                        ? std::max(1, std::min(wpb_cap, (220 * 1024) / kp.reorder_scratch_bytes))
+                        : wpb_cap;
     const int threads = 32 * wpb;
     const size_t psmem = static_cast<size_t>(wpb) * kp.reorder_scratch_bytes;
     if (psmem > 48 * 1024) {
