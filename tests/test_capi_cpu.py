@@ -159,3 +159,34 @@ def test_gp_config_defaults_follow_tab_sr_params():
     c = GPConfig()
     assert (c.tournament_size, c.p_crossover, c.p_mutation, c.max_len) == (20, 0.9, 0.1, 512)
     assert c.c().func_mask == sum(1 << f for f in (0, 1, 2, 3, 4, 5, 6))
+
+
+@pytest.mark.parametrize("field,value", [
+    ("p_crossover", 1.5), ("p_mutation", -0.1), ("func_mask", 0), ("func_mask", 1 << 22), ("depth_min", 0),
+    ("depth_max", 1), ("max_len", 9000), ("n_outputs", 0), ("tournament_size", 0), ("crossover_kind", 7),
+    ("const_lo", float("nan")), ("subtree_depth", 0),
+])
+def test_gp_config_validation_host(field, value):
+    """Host-side validation of evogp_gp_config happens before any launch, so
+    it is checkable without a GPU: every bad field is E_ARG (include/evogp.h)."""
+    from paper_2501_17168_b200.gp import GPConfig
+
+    c = GPConfig(max_len=63, n_inputs=4, depth_min=2, depth_max=6).c()
+    setattr(c, field, value)
+    lib = _lib.load()
+    null = ctypes.c_void_p(0)
+    st = lib.evogp_reproduce(null, null, null, 10, 63, null, 10, 0, ctypes.byref(c), 1, null, null, null, null,
+                             null, null)
+    assert st == _lib.E_ARG
+    if field not in ("tournament_size", "crossover_kind"):  # generation ignores the variation fields
+        assert lib.evogp_generate(10, ctypes.byref(c), 1, null, null, null, null) == _lib.E_ARG
+
+
+def test_gp_config_zero_weights_rejected_only_with_mutation():
+    from paper_2501_17168_b200.gp import GPConfig
+
+    lib = _lib.load()
+    null = ctypes.c_void_p(0)
+    c = GPConfig(max_len=63, n_inputs=4, mutation_weights=(0,) * 8, p_mutation=0.1).c()
+    assert lib.evogp_reproduce(null, null, null, 10, 63, null, 10, 0, ctypes.byref(c), 1, null, null, null, null,
+                               null, null) == _lib.E_ARG
