@@ -902,7 +902,7 @@ __device__ int reorder_program(const Node* s_nodes, int n, Node* row, unsigned c
 // Returns the new length (and *depth_out), or -1 when the sizes are
 // inconsistent. Scratch after the decoded nodes: 10 L bytes.
 __device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __restrict__ urow_size, Node* row,
-                                unsigned char* scr, int L, int lane, int* depth_out) {
+                                unsigned char* scr, int L, int lane, int* depth_out, bool reorder) {
   uint16_t* sz = reinterpret_cast<uint16_t*>(scr);
   uint16_t* nd = sz + L;  // needs; later the absorbed-prefix counts by new position
   uint16_t* par = nd + L;
@@ -932,6 +932,10 @@ __device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __res
   if (!__all_sync(FULL_MASK, ok) || sz[0] != n) return -1;
   __syncwarp();
   const int nblk = (n + 31) >> 5;
+  if (!reorder) {  // fusion only: identity positions
+    for (int j = lane; j < n; j += 32) acc[j] = 0;
+    __syncwarp();
+  } else {
   // ---- bottom-up needs
   for (int b = nblk - 1; b >= 0; --b) {
     const int base = b * 32, i = base + lane;
@@ -1007,17 +1011,37 @@ __device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __res
     if (j < n) acc[j] = static_cast<int16_t>(a);
     __syncwarp();
   }
-  // ---- fusion decisions: absorbed leaves marked at their new positions
+  }
+  // ---- fusion decisions (sw bit 1: absorbs its first-visited child, bit 2:
+  // its second-visited child); absorbed leaves marked at their new positions.
+  // A node absorbs its first-visited child when that is a leaf; a binary node
+  // whose first-visited child is not a leaf absorbs its second-visited child
+  // when that is a leaf (operand b is then the leaf, under the unreversed
+  // op: g(F1, leaf)). The last node is never absorbed (it starts the stack).
   for (int j = lane; j < n; j += 32) {
     const uint32_t op = s_nodes[j + 1].w0 & 0xFFu;
     if (op <= OP_VAR) continue;
     const int ar = func_arity(static_cast<int>(op) - OP_FN);
     if (ar > 2) continue;
     const int c1 = j + 1;
-    const int f1 = (ar == 2 && sw[j]) ? c1 + sz[c1] : c1;
-    if ((s_nodes[f1 + 1].w0 & 0xFFu) > OP_VAR) continue;
-    const int pos = f1 + acc[f1];
-    if (pos != n - 1) absd[pos] = 1;
+    const bool swp = ar == 2 && (sw[j] & 1);
+    const int f1 = swp ? c1 + sz[c1] : c1;
+    const int pos1 = f1 + acc[f1];
+    if ((s_nodes[f1 + 1].w0 & 0xFFu) <= OP_VAR) {
+      if (pos1 != n - 1) {
+        absd[pos1] = 1;
+        sw[j] |= 2;
+      }
+      continue;
+    }
+    if (ar == 2) {
+      const int f2 = swp ? c1 : c1 + sz[c1];
+      const int pos2 = f2 + acc[f2];
+      if ((s_nodes[f2 + 1].w0 & 0xFFu) <= OP_VAR && pos2 != n - 1) {
+        absd[pos2] = 1;
+        sw[j] |= 4;
+      }
+    }
   }
   __syncwarp();
   // exclusive prefix count of the absorbed positions -> nd[q]
@@ -1038,20 +1062,21 @@ __device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __res
     const uint32_t op = x.w0 & 0xFFu;
     if (op > OP_VAR) {
       const int ar = func_arity(static_cast<int>(op) - OP_FN);
-      const bool swp = ar == 2 && sw[j];
+      const uint8_t fl = sw[j];
+      const bool swp = ar == 2 && (fl & 1);
       uint32_t g = swp ? reversed_op(op) : op;
-      if (ar <= 2) {
+      if (ar <= 2 && (fl & 6)) {
         const int c1 = j + 1;
-        const int f1 = swp ? c1 + sz[c1] : c1;
-        if (absd[f1 + acc[f1]] && (s_nodes[f1 + 1].w0 & 0xFFu) <= OP_VAR) {
-          // f(leaf, top) as f_R(top, leaf); a unary node keeps its op
-          const Node l = s_nodes[f1 + 1];
-          if (ar == 2) g = reversed_op(g);
-          x.w0 = (x.w0 & ~0xFFu) | g | kFuse | ((l.w0 & 0xFFu) == OP_VAR ? kFuseVar : 0u);
-          x.w1 = l.w1;
-        } else {
-          x.w0 = (x.w0 & ~0xFFu) | g;
-        }
+        const int c2 = ar == 2 ? c1 + sz[c1] : c1;
+        // first-visited absorbed: f(leaf, top) as f_R(top, leaf) (unary keeps
+        // its op); second-visited absorbed: g(top, leaf) as is
+        const int leaf = (fl & 2) ? (swp ? c2 : c1) : (swp ? c1 : c2);
+        if ((fl & 2) && ar == 2) g = reversed_op(g);
+        const Node l = s_nodes[leaf + 1];
+        x.w0 = (x.w0 & ~0xFFu) | g | kFuse | ((l.w0 & 0xFFu) == OP_VAR ? kFuseVar : 0u);
+        x.w1 = l.w1;
+      } else {
+        x.w0 = (x.w0 & ~0xFFu) | g;
       }
     }
     row[pos - nd[pos] + 1] = x;
@@ -1148,19 +1173,22 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
       Node* s_reord = s_nodes + (p.L + 1);
       ti = stage_tree_warp(p, tp, s_nodes, lane);
       const Node* prog = s_nodes;
-      if (ti.valid && ti.maxdepth - 1 > p.reorder_above) {
-        if (p.fuse) {
-          // warp-parallel reorder + fusion straight into the program row; rows
-          // with inconsistent caller sizes are fused without reordering
-          int dep = 0;
-          const int len = reorder_fuse_par(s_nodes, ti.len, p.size + tp * p.ld, row, scratch + (p.L + 1) * 8, p.L,
-                                           lane, &dep);
-          if (len > 0) {
-            ti.len = len;
-            ti.maxdepth = dep;
-            goto compiled;
-          }
-        } else {
+      if (ti.valid && p.fuse && ti.maxdepth - 1 > p.reorder_above) {
+        // warp-parallel reorder + fusion straight into the program row; rows
+        // with inconsistent caller sizes take fuse_copy (no reordering). Rows
+        // that need no reordering also take fuse_copy: the second-child fusion
+        // of reorder_fuse_par(reorder = false) measured +1-2% in the kernels
+        // but -5% on c4's whole step (the compile pass costs more than it saves)
+        int dep = ti.maxdepth;
+        const int len = reorder_fuse_par(s_nodes, ti.len, p.size + tp * p.ld, row, scratch + (p.L + 1) * 8, p.L,
+                                         lane, &dep, true);
+        if (len > 0) {
+          ti.len = len;
+          ti.maxdepth = dep;
+          goto compiled;
+        }
+      } else if (ti.valid && ti.maxdepth - 1 > p.reorder_above) {
+        {
           ti.maxdepth = reorder_program(s_nodes, ti.len, s_reord, scratch + 2 * (p.L + 1) * 8, p.L, lane);
           prog = s_reord;
         }
