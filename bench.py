@@ -614,20 +614,27 @@ def main():
 
         e2e_mode = "one pass"
         n_chunks = int(os.environ.get("EVOGP_E2E_CHUNKS", "4" if P_local >= 100_000 else "1"))
-        if cfg.n_out == 1 and axis == "pop" and world == 1 and not cfg.paired and n_chunks > 1:
-            # single-output populations: the streaming public path (copies of
-            # chunk c+1 overlap the device work of chunk c)
+        depth = min(2, int(os.environ.get("EVOGP_E2E_DEPTH", "2")))  # two host result buffers
+        if cfg.n_out == 1 and world == 1 and not cfg.paired and (n_chunks > 1 or depth > 1):
+            # single-output populations: the streaming public path. Copies of
+            # chunk c+1 overlap the device work of chunk c; with depth 2 the
+            # next step's copies (its trees AND its dataset) also overlap this
+            # step's device work, and the host waits for step i-1's MSEs after
+            # enqueuing step i.
             from paper_2501_17168_b200.stream import HostSRFitness
 
             pipe = HostSRFitness(P_local, int(h_ty.numel()), cfg.max_len, cfg.n_in, Xd, yd, chunks=n_chunks,
                                  strategy=strategy)
-            e2e_mode = f"HostSRFitness, {n_chunks} chunks on 2 streams"
+            h_res2 = [h_res, torch.empty_like(h_res).pin_memory()]
+            pending, n_sub = [], [0]
+            e2e_mode = (f"HostSRFitness, {n_chunks} chunk(s) on 2 streams, {depth} step(s) in flight "
+                        "(X and y copied every step)")
 
             def e2e_step():  # noqa: F811
-                Xd.copy_(h_X, non_blocking=True)
-                yd.copy_(h_y, non_blocking=True)
-                torch.cuda.current_stream().synchronize()
-                pipe(h_off, h_ty, h_va, h_res)
+                pending.append(pipe.submit(h_off, h_ty, h_va, h_res2[n_sub[0] & 1], X=h_X, y=h_y))
+                n_sub[0] += 1
+                while len(pending) >= max(1, depth):
+                    pending.pop(0).synchronize()  # the oldest step's MSEs are on the host
 
         for _ in range(max(1, args.warmup)):
             e2e_step()

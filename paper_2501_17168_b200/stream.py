@@ -7,6 +7,12 @@ device tensorize (evogp_tensorize_device, row a1) and the fused SR fitness
 (evogp_sr_fitness, rows a2-a7) of chunk c; each chunk's MSEs go back to the
 host as soon as they are ready. Argument marshalling and stream plumbing
 only: every step runs in libevogp.so's kernels.
+
+`submit` is the asynchronous form: it enqueues one population and returns
+the event that fires once its MSEs are on the host. The two buffer sets
+alternate across calls as well as across chunks, so while the device scores
+population i, the copies of population i+1 (including its dataset, when
+host X / y are passed) are already in flight.
 """
 from __future__ import annotations
 
@@ -46,10 +52,25 @@ class HostSRFitness:
         self.ev_free = [torch.cuda.Event() for _ in range(2)]
         for e in self.ev_free:
             e.record(self.s_comp)
+        self.Xs = self.ys = None  # per-call dataset buffers (submit with host X / y), alternating
+        self.ev_dfree = [torch.cuda.Event() for _ in range(2)]
+        for e in self.ev_dfree:
+            e.record(self.s_comp)
+        self.k = 0  # chunk buffer-set counter, continued across calls
+        self.kc = 0  # call counter (dataset buffer set)
 
-    def __call__(self, offsets, types, values, out):
+    def __call__(self, offsets, types, values, out, X=None, y=None):
         """offsets/types/values: pinned host torch tensors (CSR); out: pinned
         host float64 tensor [P]. Returns out (after synchronising)."""
+        self.submit(offsets, types, values, out, X, y).synchronize()
+        return out
+
+    def submit(self, offsets, types, values, out, X=None, y=None):
+        """Enqueue one population without synchronising; returns the CUDA event
+        recorded after its last MSE reached `out`. X / y (pinned host tensors,
+        optional): this population's dataset, copied with its trees; default:
+        the device X / y given at construction. `out` must not be read, nor the
+        inputs changed, before the event fires."""
         import torch
 
         from . import _LIB, EvogpError, sr_fitness
@@ -57,11 +78,25 @@ class HostSRFitness:
         P = int(offsets.numel()) - 1
         off_np = offsets.numpy()
         bounds = [min(P, c * self.pc) for c in range(self.chunks + 1)]
+        if X is not None and self.Xs is None:
+            self.Xs = [torch.empty_like(self.X) for _ in range(2)]
+            self.ys = [torch.empty_like(self.y) for _ in range(2)]
+        done = torch.cuda.Event()
+        Xd, yd = self.X, self.y
+        db = self.kc & 1
+        self.kc += 1
+        if X is not None:
+            Xd, yd = self.Xs[db], self.ys[db]
+            with torch.cuda.stream(self.s_copy):  # ordered before every chunk's copies below
+                self.s_copy.wait_event(self.ev_dfree[db])
+                Xd.copy_(X, non_blocking=True)
+                yd.copy_(y, non_blocking=True)
         for c in range(self.chunks):
             p0, p1 = bounds[c], bounds[c + 1]
             if p1 <= p0:
                 continue
-            b = c & 1
+            b = self.k & 1
+            self.k += 1
             n0, n1 = int(off_np[p0]), int(off_np[p1])
             with torch.cuda.stream(self.s_copy):
                 self.s_copy.wait_event(self.ev_free[b])
@@ -83,9 +118,10 @@ class HostSRFitness:
                 if st != OK:
                     raise EvogpError(st, "evogp_tensorize_device")
                 m = self.mse[b][: p1 - p0]
-                sr_fitness(t, v, s, self.X, self.y, strategy=self.strategy, out=m, workspace=self.ws[b],
+                sr_fitness(t, v, s, Xd, yd, strategy=self.strategy, out=m, workspace=self.ws[b],
                            stream=self.s_comp)
                 out[p0:p1].copy_(m, non_blocking=True)
                 self.ev_free[b].record(self.s_comp)
-        self.s_comp.synchronize()
-        return out
+        self.ev_dfree[db].record(self.s_comp)
+        done.record(self.s_comp)
+        return done

@@ -104,3 +104,36 @@ def test_host_streaming_sr_fitness_matches_one_pass(chunks):
         out.fill_(-1.0)
         got = pipe(h_off, h_ty, h_va, out).numpy()
         assert (got.view(np.uint64) == ref.view(np.uint64)).all()
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_host_streaming_submit_two_in_flight(chunks):
+    """HostSRFitness.submit with per-call host datasets: two populations (each
+    with its own X / y) in flight at once, then a third reusing the first
+    call's buffer sets; every result equals its one-pass MSEs bit for bit."""
+    e = _e()
+    from paper_2501_17168_b200.stream import HostSRFitness
+
+    cfg = synth.CONFIGS["c4"]
+    P = 20001
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    X, y = synth.config_data(cfg)
+    cases = []
+    for k in range(3):
+        pt = synth.trees(cfg.seed + k, 0, P, cfg.max_len, synth.M_PAPER, cfg.n_in)
+        Xk, yk = (X * (1.0 + 0.25 * k)).astype(np.float32), (y - 0.5 * k).astype(np.float32)
+        Xd, yd = torch.from_numpy(Xk).cuda(), torch.from_numpy(yk).cuda()
+        h = [torch.from_numpy(a).cuda() for a in e.tensorize(pt.offsets, pt.types, pt.values, cfg.max_len, cfg.n_in)]
+        ref = e.sr_fitness(*h, Xd, yd).cpu().numpy()
+        cases.append((pin(pt.offsets.astype(np.int64)), pin(pt.types), pin(pt.values), pin(Xk), pin(yk), ref))
+    nodes = max(int(c[1].numel()) for c in cases)
+    pipe = HostSRFitness(P, nodes, cfg.max_len, cfg.n_in, torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(),
+                         chunks=chunks)
+    outs = [torch.full((P,), -1.0, dtype=torch.float64).pin_memory() for _ in cases]
+    evs = [pipe.submit(*c[:3], outs[i], X=c[3], y=c[4]) for i, c in enumerate(cases[:2])]
+    evs[0].synchronize()
+    evs.append(pipe.submit(*cases[2][:3], outs[2], X=cases[2][3], y=cases[2][4]))
+    for ev, out, c in zip(evs, outs, cases):
+        ev.synchronize()
+        got = out.numpy()
+        assert (got.view(np.uint64) == c[5].view(np.uint64)).all()
