@@ -613,7 +613,7 @@ def main():
             torch.cuda.current_stream().synchronize()
 
         e2e_mode = "one pass"
-        n_chunks = int(os.environ.get("EVOGP_E2E_CHUNKS", "4" if P_local >= 100_000 else "1"))
+        n_chunks = int(os.environ.get("EVOGP_E2E_CHUNKS", "1"))  # with 2 steps in flight, chunking measured no gain (c4) or a loss (c2)
         depth = min(2, int(os.environ.get("EVOGP_E2E_DEPTH", "2")))  # two host result buffers
         if cfg.n_out == 1 and world == 1 and not cfg.paired and (n_chunks > 1 or depth > 1):
             # single-output populations: the streaming public path. Copies of
