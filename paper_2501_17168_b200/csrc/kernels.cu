@@ -310,7 +310,14 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
         RES(k) = fabsf(a) <= OK_MAX ? FAST(a) : (SLOW_EXPR);     \
       }                                                          \
     } else {                                                     \
-      bail |= !(m <= OK_MAX);                                    \
+      if constexpr (PAPER) {                                     \
+        bail |= !(m <= OK_MAX);                                  \
+      } else if (!(m <= OK_MAX)) { /* rare: re-check without the \
+        +-inf points (FAST(+-inf) is NaN, as the library's) */   \
+        float m2 = 0.0f;                                         \
+        FOR_K m2 = fmaxf(m2, fabsf(tos[k]) == kInf ? 0.0f : fabsf(tos[k])); \
+        bail |= !(m2 <= OK_MAX);                                 \
+      }                                                          \
       if (__all_sync(FULL_MASK, m <= SMALL_MAX)) {               \
         FOR_K RES(k) = SMALL(tos[k]);                            \
       } else {                                                   \
@@ -435,10 +442,15 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
                                : ((a <= kSqrtRange && a >= kSqrtRangeMin) ? sqrt_fast(a) : slow_sqrt(a));
           }
         } else {
-          bail |= !(mx <= kSqrtRange) || mn < __float_as_uint(kSqrtRangeMin) - 1u;
+          if (!(mx <= kSqrtRange)) {  // rare: re-check without the inf points (sqrt(inf) = inf, selected below)
+            float m2 = 0.0f;
+            FOR_K m2 = fmaxf(m2, fabsf(tos[k]) == kInf ? 0.0f : fabsf(tos[k]));
+            bail |= !(m2 <= kSqrtRange);
+          }
+          bail |= mn < __float_as_uint(kSqrtRangeMin) - 1u;
           FOR_K {
             const float a = fabsf(tos[k]);
-            RES(k) = a == 0.0f ? 0.0f : sqrt_fast(a);
+            RES(k) = (a == 0.0f || a == kInf) ? a : sqrt_fast(a);  // = slow_sqrt at 0 and inf
           }
         }
         MODI_FIN(tos)
@@ -454,8 +466,15 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
             RES(k) = fabsf(a) > kDelta ? (fabsf(a) <= kSqrtRange ? rcp_fast(a) : slow_rcp(a)) : 0.0f;
           }
         } else {
-          bail |= !(mx <= kSqrtRange);
-          FOR_K RES(k) = fabsf(tos[k]) > kDelta ? rcp_fast(tos[k]) : 0.0f;
+          if (!(mx <= kSqrtRange)) {  // rare: re-check without the +-inf points (1 / +-inf = +-0, selected below)
+            float m2 = 0.0f;
+            FOR_K m2 = fmaxf(m2, fabsf(tos[k]) == kInf ? 0.0f : fabsf(tos[k]));
+            bail |= !(m2 <= kSqrtRange);
+          }
+          FOR_K {
+            const float a = tos[k];
+            RES(k) = fabsf(a) > kDelta ? (fabsf(a) == kInf ? copysignf(0.0f, a) : rcp_fast(a)) : 0.0f;
+          }
         }
         MODI_FIN(tos)
         break;

@@ -507,6 +507,46 @@ def test_ieee_fast_paths_bitexact():
             assert ok.all(), (name, strategy, (~ok).sum(), X[~ok][:3], g[row][~ok][:3], ref[row][~ok][:3])
 
 
+def test_infinite_operands_stay_on_the_hot_path():
+    """In full-set rows, SIN, COS, TAN, INV and SQRT at +-inf take the fast
+    (hot) copy instead of re-running the chunk cold: trig gives NaN (as sinf / cosf / tanf), INV
+    gives +-0 and SQRT inf, exactly; the finite points keep their values.
+    Every point is in the fast range or infinite, so nothing else bails."""
+    rng = np.random.default_rng(77)
+    D = 4099
+    a = rng.uniform(-3.0, 3.0, D).astype(np.float32)
+    a[::7] = np.inf
+    a[3::7] = -np.inf
+    X = np.ascontiguousarray(a[:, None])
+    # SIN, COS, TAN of NEG(x0) (NEG keeps the rows off the paper-set copy,
+    # which still bails on inf), INV(NEG(x0)), SQRT(NEG(x0))
+    fns = (4, 5, 6, 16, 15)
+    pt = synth.PrefixTrees(np.arange(0, 3 * len(fns) + 1, 3, dtype=np.int64),
+                           np.array([2, 2, 1] * len(fns), np.int16),
+                           np.array([v for f in fns for v in (f, 13, 0)], np.float32))
+    dt = to_device(pt, 3, 1)
+    a = -a  # the operand the functions see (X holds -a)
+    inf = np.isinf(a)
+    with np.errstate(all="ignore"):
+        inv = np.where(np.abs(a) > np.float32(0.001), np.float32(1) / a, np.float32(0)).astype(np.float32)
+        sq = np.sqrt(np.abs(a)).astype(np.float32)
+    evogp = _evogp()
+    for strategy in ("inter", "intra"):
+        ws = evogp.Workspace(len(fns), D, 3, 1, 1, device="cuda")
+        t, v, s_ = dt
+        g = evogp.eval(t, v, s_, torch.from_numpy(X).cuda(), strategy=strategy, workspace=ws)
+        torch.cuda.synchronize()
+        g = g.cpu().numpy()[:, :, 0]
+        off = ws.ptr - ws.buf.data_ptr()
+        assert int(ws.buf[off + 4: off + 8].view(torch.int32).item()) == 0, strategy  # no chunk re-ran cold
+        for row, fn in enumerate((np.sin, np.cos, np.tan)):
+            assert np.isnan(g[row][inf]).all(), (fn.__name__, strategy)
+            ref = fn(a[~inf].astype(np.float64))
+            assert (np.abs(g[row][~inf] - ref) <= 1e-5 * np.maximum(1.0, np.abs(ref))).all(), (fn.__name__, strategy)
+        assert (g[3].astype(np.float32).view(np.uint32) == inv.view(np.uint32)).all(), strategy  # +-0 at +-inf
+        assert (g[4].astype(np.float32).view(np.uint32) == sq.view(np.uint32)).all(), strategy
+
+
 @pytest.mark.parametrize("warps", ["48", "64"])
 def test_reordered_programs_bitexact(warps, monkeypatch):
     """With a tiny shared-memory stack (many warps per SM) the compile pass
