@@ -356,11 +356,28 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
         RES(k) = fabsf(de) > kDelta ? (fast ? div_fast(nu, de) : slow_div(nu, de)) : 1.0f; \
       }                                                                             \
     } else {                                                                        \
-      bail |= !(mx <= kDivRange);                                                   \
+      bool with_inf = false;                                                        \
+      if constexpr (PAPER) {                                                        \
+        bail |= !(mx <= kDivRange);                                                 \
+      } else if (!(mx <= kDivRange)) { /* rare: re-check without the +-inf */       \
+        float m2 = 0.0f;                                                            \
+        FOR_K m2 = fmaxf(m2, fmaxf(fabsf(tos[k]) == kInf ? 0.0f : fabsf(tos[k]),    \
+                                   fabsf(b[k]) == kInf ? 0.0f : fabsf(b[k])));      \
+        bail |= !(m2 <= kDivRange);                                                 \
+        with_inf = true;                                                            \
+      }                                                                             \
       if (mn < kDivRangeMin) {                                                      \
         FOR_K bail |= NUM[k] != 0.0f && fabsf(NUM[k]) < kDivRangeMin;               \
       }                                                                             \
-      FOR_K RES(k) = fabsf(DEN[k]) > kDelta ? div_fast(NUM[k], DEN[k]) : 1.0f;      \
+      if (with_inf) { /* an inf operand: nu * rcp(de) is the IEEE quotient */       \
+        FOR_K {                                                                     \
+          const float nu = NUM[k], de = DEN[k];                                     \
+          const bool inf = fabsf(nu) == kInf || fabsf(de) == kInf;                  \
+          RES(k) = fabsf(de) > kDelta ? (inf ? __fmul_rn(nu, rcp_approx(de)) : div_fast(nu, de)) : 1.0f; \
+        }                                                                           \
+      } else {                                                                      \
+        FOR_K RES(k) = fabsf(DEN[k]) > kDelta ? div_fast(NUM[k], DEN[k]) : 1.0f;    \
+      }                                                                             \
     }                                                                               \
     MODI_FIN(b)                                                                     \
     break;                                                                          \

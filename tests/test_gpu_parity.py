@@ -508,9 +508,10 @@ def test_ieee_fast_paths_bitexact():
 
 
 def test_infinite_operands_stay_on_the_hot_path():
-    """In full-set rows, SIN, COS, TAN, INV and SQRT at +-inf take the fast
+    """In full-set rows, SIN, COS, TAN, INV, SQRT and DIV at +-inf take the fast
     (hot) copy instead of re-running the chunk cold: trig gives NaN (as sinf / cosf / tanf), INV
-    gives +-0 and SQRT inf, exactly; the finite points keep their values.
+    gives +-0, SQRT inf and DIV the IEEE quotient, exactly; the finite points
+    keep their values.
     Every point is in the fast range or infinite, so nothing else bails."""
     rng = np.random.default_rng(77)
     D = 4099
@@ -520,19 +521,24 @@ def test_infinite_operands_stay_on_the_hot_path():
     X = np.ascontiguousarray(a[:, None])
     # SIN, COS, TAN of NEG(x0) (NEG keeps the rows off the paper-set copy,
     # which still bails on inf), INV(NEG(x0)), SQRT(NEG(x0))
+    # plus DIV(NEG(x0), 0.5) (inf / finite) and DIV(2.5, NEG(x0)) (finite / inf)
     fns = (4, 5, 6, 16, 15)
-    pt = synth.PrefixTrees(np.arange(0, 3 * len(fns) + 1, 3, dtype=np.int64),
-                           np.array([2, 2, 1] * len(fns), np.int16),
-                           np.array([v for f in fns for v in (f, 13, 0)], np.float32))
-    dt = to_device(pt, 3, 1)
+    rows_t = [[2, 2, 1]] * len(fns) + [[3, 2, 1, 0], [3, 0, 2, 1]]
+    rows_v = [[f, 13, 0] for f in fns] + [[3, 13, 0, 0.5], [3, 2.5, 13, 0]]
+    pt = synth.PrefixTrees(np.cumsum([0] + [len(r) for r in rows_t]).astype(np.int64),
+                           np.array([x for r in rows_t for x in r], np.int16),
+                           np.array([x for r in rows_v for x in r], np.float32))
+    dt = to_device(pt, 4, 1)
     a = -a  # the operand the functions see (X holds -a)
     inf = np.isinf(a)
     with np.errstate(all="ignore"):
         inv = np.where(np.abs(a) > np.float32(0.001), np.float32(1) / a, np.float32(0)).astype(np.float32)
         sq = np.sqrt(np.abs(a)).astype(np.float32)
+        dv1 = (a / np.float32(0.5)).astype(np.float32)
+        dv2 = np.where(np.abs(a) > np.float32(0.001), np.float32(2.5) / a, np.float32(1)).astype(np.float32)
     evogp = _evogp()
     for strategy in ("inter", "intra"):
-        ws = evogp.Workspace(len(fns), D, 3, 1, 1, device="cuda")
+        ws = evogp.Workspace(len(rows_t), D, 4, 1, 1, device="cuda")
         t, v, s_ = dt
         g = evogp.eval(t, v, s_, torch.from_numpy(X).cuda(), strategy=strategy, workspace=ws)
         torch.cuda.synchronize()
@@ -545,6 +551,8 @@ def test_infinite_operands_stay_on_the_hot_path():
             assert (np.abs(g[row][~inf] - ref) <= 1e-5 * np.maximum(1.0, np.abs(ref))).all(), (fn.__name__, strategy)
         assert (g[3].astype(np.float32).view(np.uint32) == inv.view(np.uint32)).all(), strategy  # +-0 at +-inf
         assert (g[4].astype(np.float32).view(np.uint32) == sq.view(np.uint32)).all(), strategy
+        assert (g[5].astype(np.float32).view(np.uint32) == dv1.view(np.uint32)).all(), strategy  # +-inf
+        assert (g[6].astype(np.float32).view(np.uint32) == dv2.view(np.uint32)).all(), strategy  # +-0
 
 
 @pytest.mark.parametrize("warps", ["48", "64"])
