@@ -6,13 +6,27 @@ LIB := $(PKG)/libevogp.so
 # IEEE-faithful FP32 on the parity path: no fast math, no FTZ, IEEE div/sqrt (R5)
 NVFLAGS := -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
            -ftz=false -prec-div=true -prec-sqrt=true -Xcompiler -fPIC,-O2 -Xptxas -v
-SRCS := $(CSRC)/kernels.cu $(CSRC)/paired.cu $(CSRC)/variation.cu $(CSRC)/tensorize_dev.cu $(CSRC)/capi.cu $(CSRC)/tensorize.cpp
-HDRS := $(CSRC)/evogp_internal.h $(CSRC)/fastmath.cuh $(CSRC)/decode.cuh $(CSRC)/selector_table.inc include/evogp.h
+# one translation unit per evaluation-kernel family so `make -j` builds them in parallel
+CU := eval_inter_k8 eval_inter_k4 eval_inter_k2 eval_inter_k1 eval_intra_k8 eval_intra_k4 compile plan \
+      paired variation tensorize_dev capi
+OBJDIR := build/obj
+OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU))) $(OBJDIR)/tensorize.o
+HDRS := $(CSRC)/evogp_internal.h $(CSRC)/fastmath.cuh $(CSRC)/decode.cuh $(CSRC)/interp.cuh \
+        $(CSRC)/selector_table.inc include/evogp.h
 
 all: $(LIB) oracle/liboracle.so synth/libsynth.so
 
-$(LIB): $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) 2> $(PKG)/ptxas.log || (cat $(PKG)/ptxas.log; exit 1)
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $@.ptxas.log || (cat $@.ptxas.log; exit 1)
+
+$(OBJDIR)/tensorize.o: $(CSRC)/tensorize.cpp $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+$(LIB): $(OBJS)
+	$(NVCC) -gencode arch=compute_100a,code=sm_100a -shared -o $@ $(OBJS) -lcudart
+	cat $(OBJDIR)/*.ptxas.log > $(PKG)/ptxas.log
 
 # test infrastructure (never linked into the product)
 oracle/liboracle.so: oracle/oracle.c oracle/variation.c
@@ -22,6 +36,6 @@ synth/libsynth.so: synth/synth.c
 	gcc -O2 -fPIC -shared -pthread -o $@ $< -lm
 
 clean:
-	rm -f $(LIB) oracle/liboracle.so synth/libsynth.so $(PKG)/ptxas.log
+	rm -rf $(LIB) oracle/liboracle.so synth/libsynth.so $(PKG)/ptxas.log $(OBJDIR)
 
 .PHONY: all clean

@@ -41,7 +41,6 @@ import synth  # noqa: E402  (seeded inputs; no method arithmetic)
 METRIC = "GPops/s (nodes × datapoints / s) at 1/2/4/8 B200, % of FP32/SFU roofline"
 UNIT = "GPops/s"
 SFU_FUNCS = (3, 4, 5, 6, 9, 10, 11, 12, 15, 16)  # DIV SIN COS TAN POW LOG EXP TANH SQRT INV (R3)
-SMS = 148
 FP32_LANES = 128  # per SM per clock
 SFU_LANES = 16  # per SM per clock (measured 15.9, profiles/microbench_pipes_r01.json)
 
@@ -52,7 +51,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(synth.CONFIGS), default="c2")
+    ap.add_argument("--config", choices=sorted(synth.CONFIGS), default="c3")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="population axis: strong = one population of P trees sharded over the ranks "
+                         "(SURVEY §8(e)); weak = P trees per rank")
     ap.add_argument("--mix", choices=sorted(synth.MIXES), default=None)
     ap.add_argument("--strategy", choices=["auto", "inter", "intra"], default="auto")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -94,15 +96,31 @@ def tree_stats(pt):
     return int(lens.sum()), float(sfu) / max(1, len(pt.types))
 
 
-def local_shards(cfg, rank, world):
-    """c3: datapoint-sharded (strong scaling: fixed total D); others:
-    population-sharded with P trees per rank (weak scaling)."""
-    if cfg.index == 3:
-        from paper_2501_17168_b200.dist import shard_rows
+def local_shards(cfg, rank, world, scaling="strong"):
+    """c3: datapoint-sharded (strong scaling: fixed total D). Others:
+    population-sharded; strong = one population of cfg.P trees, rank r owns
+    rows shard_rows(P, world, r); weak = cfg.P trees per rank."""
+    from paper_2501_17168_b200.dist import shard_rows
 
+    if cfg.index == 3:
         d0, d1 = shard_rows(cfg.D, world, rank)
         return "data", (0, cfg.P), (d0, d1)
-    return "pop", (rank * cfg.P, (rank + 1) * cfg.P), (0, cfg.D)
+    if scaling == "weak":
+        return "pop", (rank * cfg.P, (rank + 1) * cfg.P), (0, cfg.D)
+    return "pop", shard_rows(cfg.P, world, rank), (0, cfg.D)
+
+
+def relaunch_distributed(n):
+    """`bench.py --gpus N` run as a plain command: re-exec under torchrun with
+    N ranks (one per GPU, NCCL) and pass its exit status through."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ---------------------------------------------------------------- clocks
@@ -222,7 +240,8 @@ def run_reference(args, cfg, mix):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
-        "scaling": "weak" if cfg.index != 3 else "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak" if args.scaling == "weak" and cfg.index != 3 else "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_desc(cfg, mix), "parallelism": "host threads (oracle)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
                          "sample": "each step: " + desc},
@@ -433,6 +452,7 @@ def run_loop(args, cfg):
         n_sfu = torch.isin(vals, torch.tensor(SFU_FUNCS, device=dev)).sum().item()
         n_nodes = (s[:, 0].to(torch.int64)).sum().item()
         sfu_frac = n_sfu / max(1, n_nodes)
+        SMS = torch.cuda.get_device_properties(dev).multi_processor_count
         roof = 1.0 / max(1.0 / (SMS * FP32_LANES * f), sfu_frac / (SMS * SFU_LANES * f))
         achieved = work_local / (kern_ms * 1e-3)
         line = {
@@ -471,6 +491,8 @@ def run_loop(args, cfg):
 # ---------------------------------------------------------------- our arm
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args.gpus)
     cfg = synth.CONFIGS[args.config]
     mix = args.mix or default_mix(cfg)
     if cfg.loop:
@@ -486,14 +508,16 @@ def main():
 
     rank, world, local = dist_env()
     if world != args.gpus:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # under torchrun (even one rank) the sharded path + NCCL combine runs
+    use_dist = world > 1 or "WORLD_SIZE" in os.environ
+    if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
 
-    axis, (p0, p1), (d0, d1) = local_shards(cfg, rank, world)
+    axis, (p0, p1), (d0, d1) = local_shards(cfg, rank, world, args.scaling)
     pt = synth.trees(cfg.seed, p0, p1 - p0, cfg.max_len, synth.MIXES[mix], cfg.n_in, cfg.n_out, cfg.modi_prob)
     if cfg.paired:  # NEXT-2: every individual's own B observations, rows p0*B ...
         X, y = synth.config_data(cfg, p0 * cfg.D, (p1 - p0) * cfg.D)
@@ -516,8 +540,11 @@ def main():
     if cfg.paired:
         out_eval = torch.empty(((P_local, cfg.n_out) if cfg.D == 1 else (P_local, cfg.D, cfg.n_out)),
                                dtype=torch.float32, device=dev)
-    mse_local = torch.full((P_local,), float("nan"), dtype=torch.float64, device=dev)
-    P_total = cfg.P * world if axis == "pop" else cfg.P
+    P_total = cfg.P * world if (axis == "pop" and args.scaling == "weak") else cfg.P
+    # population axis: the rank's MSEs go into its equal-size all-gather slot
+    slot = edist.padded_shard(P_total, world) if (axis == "pop" and use_dist) else P_local
+    mse_slot = torch.full((slot,), float("nan"), dtype=torch.float64, device=dev)
+    mse_local = mse_slot[:P_local]
 
     def step():
         if cfg.paired:
@@ -527,20 +554,20 @@ def main():
             evogp.eval(td, vd, sd, Xd, n_outputs=cfg.n_out, strategy=strategy, out=out_eval, workspace=ws)
             return out_eval
         if axis == "data":
-            if world == 1:
+            if not use_dist:
                 return evogp.sr_fitness(td, vd, sd, Xd, yd, strategy=strategy, out=mse_local, workspace=ws)
             return edist.sr_fitness_data_sharded(
                 td, vd, sd, Xd, yd, cfg.D, out=mse_local,
                 sse_fn=lambda a, b, c, x, yy, o: evogp.sr_sse(a, b, c, x, yy, strategy=strategy, out=o, workspace=ws))
-        if world == 1:
+        if not use_dist:
             return evogp.sr_fitness(td, vd, sd, Xd, yd, strategy=strategy, out=mse_local, workspace=ws)
         return edist.sr_fitness_population_sharded(
-            td, vd, sd, Xd, yd, P_total, local_out=mse_local,
+            td, vd, sd, Xd, yd, P_total, local_out=mse_slot,
             fitness_fn=lambda a, b, c, x, yy, o: evogp.sr_fitness(a, b, c, x, yy, strategy=strategy, out=o,
                                                                   workspace=ws))
 
     def barrier():
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -582,12 +609,43 @@ def main():
     cold_chunks = int(ws.buf[off + 4: off + 8].view(torch.int32).item())
     tt = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device=dev)
     work = torch.tensor([float(nodes) * D_local], dtype=torch.float64, device=dev)
-    if world > 1:
+    if use_dist:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dist.all_reduce(work, op=dist.ReduceOp.SUM)
     step_ms, kern_ms = tt.tolist()
     total_work = work.item()  # node x datapoint evaluations per step, all ranks
     value = total_work * args.steps / (step_ms * 1e-3)
+
+    # ---- launch-bound configs (c1): the same step replayed from a CUDA graph
+    # (SURVEY §8(d) config 1): G steps captured once, the graph replayed K
+    # times; value = G * K * work / device time of the replays
+    graph = None
+    if cfg.index == 1 and world == 1 and not cfg.paired:
+        G = 100
+        gs = torch.cuda.Stream(device=dev)
+        gs.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(gs):
+            for _ in range(3):
+                step()  # plan caches, occupancy queries, function attributes
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=gs):
+            for _ in range(G):
+                step()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(args.steps):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        gms = a.elapsed_time(b)
+        graph = {"value": total_work * G * args.steps / (gms * 1e-3), "unit": UNIT, "steps_per_graph": G,
+                 "replays": args.steps, "us_per_step": gms * 1e3 / (G * args.steps),
+                 "note": "CUDA-graph-batched replay of the same step (launch-bound config); the graph's kernels "
+                         "are the same two launches per step, no L2 flush between graph steps"}
 
     # ---- e2e: host prefix lists -> tensorize -> H2D -> device call -> D2H
     e2e = None
@@ -615,7 +673,7 @@ def main():
         e2e_mode = "one pass"
         n_chunks = int(os.environ.get("EVOGP_E2E_CHUNKS", "1"))  # with 2 steps in flight, chunking measured no gain (c4) or a loss (c2)
         depth = min(2, int(os.environ.get("EVOGP_E2E_DEPTH", "2")))  # two host result buffers
-        if cfg.n_out == 1 and world == 1 and not cfg.paired and (n_chunks > 1 or depth > 1):
+        if cfg.n_out == 1 and not use_dist and not cfg.paired and (n_chunks > 1 or depth > 1):
             # single-output populations: the streaming public path. Copies of
             # chunk c+1 overlap the device work of chunk c; with depth 2 the
             # next step's copies (its trees AND its dataset) also overlap this
@@ -644,7 +702,7 @@ def main():
             e2e_step()
         barrier()
         el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        if world > 1:
+        if use_dist:
             dist.all_reduce(el, op=dist.ReduceOp.MAX)
         e2e = {"value": total_work * args.steps / el.item(), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
@@ -654,6 +712,7 @@ def main():
     if rank == 0:
         peaks, peak_src = measured_peaks()
         f = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        SMS = torch.cuda.get_device_properties(dev).multi_processor_count
         r_fp32 = SMS * FP32_LANES * f
         r_sfu = SMS * SFU_LANES * f
         roof = 1.0 / max(1.0 / r_fp32, sfu_frac / r_sfu)  # per GPU
@@ -666,32 +725,51 @@ def main():
             alg_bytes = 6.0 * nodes + 2.0 * P_local + 4.0 * P_local * cfg.D * (cfg.n_in + cfg.n_out)
             hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
             gbs = alg_bytes * args.steps / (kern_ms * 1e-3) / 1e9
-        traffic = None
+        # DRAM traffic of the dominant kernel from the committed `ncu --set
+        # full` capture of this config (a profiler number: never taken here)
+        traffic, traffic_src = None, None
         prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}_{chosen}_summary.json")
         if os.path.exists(prof):
             with open(prof) as fh:
-                traffic = json.load(fh).get("dram_bytes_per_launch")
+                pj = json.load(fh)
+            traffic, traffic_src = pj.get("dram_bytes_per_launch"), f"profiles/{os.path.basename(prof)} ({pj.get('note', '')})"
+        hbm_view = None
+        if cfg.n_out > 1 and not cfg.paired:
+            # multi-output eval: the P x D x n_out FP32 output store is the one
+            # HBM-relevant stream: report it against HBM
+            out_bytes = 4.0 * P_local * D_local * cfg.n_out
+            alg_bytes_n = out_bytes + 8.0 * nodes + 4.0 * D_local * cfg.n_in
+            hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+            gbs_n = alg_bytes_n * args.steps / (kern_ms * 1e-3) / 1e9
+            hbm_view = {"achieved": gbs_n, "peak": hbm_peak, "unit": "GB/s", "frac": gbs_n / hbm_peak,
+                        "algorithmic_bytes_per_launch": alg_bytes_n, "output_bytes_per_launch": out_bytes,
+                        "peak_basis": f"hbm_gbs ({peak_src})"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if axis == "data" else "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if (axis == "data" or args.scaling == "strong") else "weak", "vs_baseline": None,
+            "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": workload_desc(cfg, mix), "P_per_rank": P_local, "D_per_rank": D_local,
+            "config": {"workload": workload_desc(cfg, mix), "P_total": P_total, "P_per_rank": P_local,
+                       "D_per_rank": D_local,
                        "max_len": cfg.max_len, "n_inputs": cfg.n_in, "n_outputs": cfg.n_out,
                        "mean_len": nodes / max(1, P_local), "sfu_node_fraction": sfu_frac,
-                       "strategy": chosen, "parallelism": f"{axis}-shard x{world}",
+                       "strategy": chosen,
+                       "parallelism": f"{axis}-shard x{world}" + (" (NCCL)" if use_dist else " (no collective)"),
                        "cold_rerun_chunks_last_step": cold_chunks,
                        "l2": "flushed (256 MiB write) before every timed step",
                        "step": ("evogp_eval_paired" if cfg.paired else
                                 "evogp_eval" if cfg.n_out > 1 else "evogp_sr_fitness") +
-                               (" + NCCL combine" if world > 1 else "")},
+                               (" + NCCL combine" if use_dist and cfg.n_out == 1 and not cfg.paired else "")},
             "roofline": ({"bound": "alu", "achieved": achieved, "peak": roof, "unit": UNIT, "frac": achieved / roof,
-                          "traffic": traffic, "kernel": f"k_{chosen}",
+                          "traffic": traffic, "traffic_source": traffic_src, "kernel": f"k_{chosen}",
                           "peak_basis": f"{SMS} SMs x min({FP32_LANES} FP32, {SFU_LANES}/s MUFU) lanes/clk at "
-                                        f"sm_max_mhz={f / 1e6:.0f} ({peak_src}), s={sfu_frac:.3f}"}
+                                        f"sm_max_mhz={f / 1e6:.0f} ({peak_src}), s={sfu_frac:.3f}",
+                          **({"hbm_view": hbm_view} if hbm_view else {})}
                          if not cfg.paired else
                          {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
-                          "traffic": traffic, "kernel": "k_paired", "algorithmic_bytes_per_launch": alg_bytes,
+                          "traffic": traffic, "traffic_source": traffic_src, "kernel": "k_paired",
+                          "algorithmic_bytes_per_launch": alg_bytes,
                           "alu_view": {"achieved": achieved, "unit": UNIT, "fp32_sfu_roof": roof,
                                        "frac": achieved / roof},
                           "peak_basis": f"hbm_gbs ({peak_src})"}),
@@ -699,12 +777,14 @@ def main():
             "clocks": clocks,
             "e2e": e2e,
         }
+        if graph is not None:
+            line["graph_replay"] = graph
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
             cv, desc = time_oracle(cfg, mix, args.cpu_seconds, threads)
             line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
     return 0

@@ -23,7 +23,7 @@ _LIB = _lib.load()
 
 __all__ = [
     "tensorize", "tensorize_device", "eval", "sr_fitness", "sr_sse", "classification_accuracy", "eval_paired", "select_strategy", "workspace_size", "Workspace",
-    "check_device_flags", "EvogpError", "last_launch_count", "set_kernel_timing", "STRATEGIES",
+    "check_device_flags", "EvogpError", "last_launch_count", "set_tuning", "set_kernel_timing", "STRATEGIES",
     "GPConfig", "generate", "subtree_exchange", "tournament", "reproduce", "Evolution",
 ]
 
@@ -105,13 +105,16 @@ def workspace_size(P: int, D: int, max_len: int, n_inputs: int, n_outputs: int =
 
 
 class Workspace:
-    """Zero-initialised device scratch sized by evogp_workspace_size."""
+    """Zero-initialised device scratch sized by evogp_workspace_size (for the
+    device it lives on, under the current tuning)."""
 
     def __init__(self, P, D, max_len, n_inputs, n_outputs=1, device=None):
         import torch
 
-        self.nbytes = workspace_size(P, D, max_len, n_inputs, n_outputs)
-        self.buf = torch.zeros(self.nbytes + 256, dtype=torch.uint8, device=device)
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        with torch.cuda.device(dev):
+            self.nbytes = workspace_size(P, D, max_len, n_inputs, n_outputs)
+        self.buf = torch.zeros(self.nbytes + 256, dtype=torch.uint8, device=dev)
         base = self.buf.data_ptr()
         self.ptr = (base + 255) // 256 * 256
         self.key = (P, D, max_len, n_inputs, n_outputs, str(self.buf.device))
@@ -120,13 +123,23 @@ class Workspace:
 _WS_CACHE: dict = {}
 
 
-def _workspace(P, D, L, n_in, n_out, device, ws):
+def _workspace(P, D, L, n_in, n_out, device, ws, stream=None):
+    """The caller's workspace, else a cached one private to (shape, device,
+    stream, thread): calls sharing a workspace must be stream-ordered
+    (include/evogp.h), which a per-stream, per-thread cache guarantees."""
     if ws is not None:
         return ws
-    key = (P, D, L, n_in, n_out, str(device))
+    import threading
+
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    key = (P, D, L, n_in, n_out, str(device), int(s.cuda_stream), threading.get_ident())
     w = _WS_CACHE.get(key)
     if w is None:
         if len(_WS_CACHE) > 16:
+            # entries may still be in use by enqueued work on their streams
+            torch.cuda.synchronize(device)
             _WS_CACHE.clear()
         w = Workspace(P, D, L, n_in, n_out, device)
         _WS_CACHE[key] = w
@@ -141,23 +154,37 @@ def _stream_ptr(stream, device):
 
 
 def _tree_args(type_, value, size, max_len):
+    import torch
+
+    if type_.dim() != 2 or value.shape != type_.shape or size.shape != type_.shape:
+        raise ValueError("type / value / size must be [P, ld] arrays of the same shape")
+    for t, dt in ((type_, torch.int16), (value, torch.float32), (size, torch.int16)):
+        if not t.is_cuda or not t.is_contiguous() or t.dtype != dt:
+            raise ValueError("tree arrays must be contiguous CUDA tensors: type int16, value float32, size int16")
+        if t.device != type_.device:
+            raise ValueError("tree arrays must be on one device")
     P, ld = int(type_.shape[0]), int(type_.shape[1])
     L = ld if max_len is None else int(max_len)
-    for t in (type_, value, size):
-        if not t.is_cuda or not t.is_contiguous():
-            raise ValueError("tree arrays must be contiguous CUDA tensors")
     return P, L, ld
 
 
 def _x_args(X, x_layout):
+    import torch
+
     lay = X_SOA if x_layout in ("soa", X_SOA) else X_ROWMAJOR
-    if not X.is_cuda or not X.is_contiguous():
-        raise ValueError("X must be a contiguous CUDA tensor")
+    if not X.is_cuda or not X.is_contiguous() or X.dtype != torch.float32 or X.dim() != 2:
+        raise ValueError("X must be a contiguous 2-D float32 CUDA tensor")
     if lay == X_ROWMAJOR:
         D, n_in = int(X.shape[0]), int(X.shape[1])
     else:
         n_in, D = int(X.shape[0]), int(X.shape[1])
     return lay, D, n_in
+
+
+def _check_out(out, shape, dtype, device):
+    if out.dtype != dtype or not out.is_cuda or not out.is_contiguous() or out.device != device \
+            or out.numel() != int(np.prod(shape)):
+        raise ValueError(f"out must be a contiguous {dtype} CUDA tensor of {int(np.prod(shape))} elements on {device}")
 
 
 def eval(type_, value, size, X, n_outputs: int = 1, strategy="auto", x_layout="rowmajor", max_len=None,
@@ -169,9 +196,12 @@ def eval(type_, value, size, X, n_outputs: int = 1, strategy="auto", x_layout="r
     lay, D, n_in = _x_args(X, x_layout)
     if out is None:
         out = torch.empty((P, D, n_outputs), dtype=torch.float32, device=X.device)
-    ws = _workspace(P, D, L, n_in, n_outputs, X.device, workspace)
-    st = _LIB.evogp_eval(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(X), D, n_in, lay, n_outputs, _vp(out),
-                         STRATEGIES[strategy], ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream, X.device))
+    _check_out(out, (P, D, n_outputs), torch.float32, X.device)
+    with torch.cuda.device(X.device):
+        ws = _workspace(P, D, L, n_in, n_outputs, X.device, workspace, stream)
+        st = _LIB.evogp_eval(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(X), D, n_in, lay, n_outputs,
+                             _vp(out), STRATEGIES[strategy], ctypes.c_void_p(ws.ptr), ws.nbytes,
+                             _stream_ptr(stream, X.device))
     if st != OK:
         raise EvogpError(st, "evogp_eval")
     return out
@@ -186,9 +216,11 @@ def _sr(fn, name, type_, value, size, X, y, strategy, x_layout, max_len, out, wo
         raise ValueError("y must be a float32 CUDA tensor of length D")
     if out is None:
         out = torch.empty(P, dtype=torch.float64, device=X.device)
-    ws = _workspace(P, D, L, n_in, 1, X.device, workspace)
-    st = fn(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(X), D, n_in, lay, _vp(y), _vp(out),
-            STRATEGIES[strategy], ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream, X.device))
+    _check_out(out, (P,), torch.float64, X.device)
+    with torch.cuda.device(X.device):
+        ws = _workspace(P, D, L, n_in, 1, X.device, workspace, stream)
+        st = fn(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(X), D, n_in, lay, _vp(y), _vp(out),
+                STRATEGIES[strategy], ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream, X.device))
     if st != OK:
         raise EvogpError(st, name)
     return out
@@ -221,10 +253,12 @@ def classification_accuracy(type_, value, size, X, labels, n_classes: int, strat
         raise ValueError("labels must be an int32 CUDA tensor of length D")
     if out is None:
         out = torch.empty(P, dtype=torch.float64, device=X.device)
-    ws = _workspace(P, D, L, n_in, n_classes, X.device, workspace)
-    st = _LIB.evogp_classification_accuracy(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(X), D, n_in, lay,
-                                            n_classes, _vp(labels), _vp(out), STRATEGIES[strategy],
-                                            ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream, X.device))
+    _check_out(out, (P,), torch.float64, X.device)
+    with torch.cuda.device(X.device):
+        ws = _workspace(P, D, L, n_in, n_classes, X.device, workspace, stream)
+        st = _LIB.evogp_classification_accuracy(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(X), D, n_in, lay,
+                                                n_classes, _vp(labels), _vp(out), STRATEGIES[strategy],
+                                                ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream, X.device))
     if st != OK:
         raise EvogpError(st, "evogp_classification_accuracy")
     return out
@@ -247,9 +281,11 @@ def eval_paired(type_, value, size, obs, n_outputs: int = 1, max_len=None, out=N
     shape = (P, n_outputs) if obs.dim() == 2 else (P, B, n_outputs)
     if out is None:
         out = torch.empty(shape, dtype=torch.float32, device=obs.device)
-    ws = workspace if workspace is not None else _flags_workspace(obs.device)
-    st = _LIB.evogp_eval_paired(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(obs), B, n_in, n_outputs,
-                                _vp(out), ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream, obs.device))
+    _check_out(out, shape, torch.float32, obs.device)
+    with torch.cuda.device(obs.device):
+        ws = workspace if workspace is not None else _flags_workspace(obs.device)
+        st = _LIB.evogp_eval_paired(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(obs), B, n_in, n_outputs,
+                                    _vp(out), ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream, obs.device))
     if st != OK:
         raise EvogpError(st, "evogp_eval_paired")
     return out
@@ -278,6 +314,15 @@ def check_device_flags(workspace: Workspace, stream=None) -> int:
     if st != OK:
         raise EvogpError(st, "evogp_check_device_flags")
     return int(flags[0])
+
+
+def set_tuning(target_warps: int = 0, no_reorder: bool = False, no_fuse: bool = False, K: int = 0) -> None:
+    """evogp_set_tuning for this thread (calibration sweeps, tests); all
+    defaults = the library's own plan. Results never depend on it."""
+    t = _lib.Tuning(int(target_warps), int(bool(no_reorder)), int(bool(no_fuse)), int(K))
+    st = _LIB.evogp_set_tuning(ctypes.byref(t))
+    if st != OK:
+        raise EvogpError(st, "evogp_set_tuning")
 
 
 def last_launch_count() -> int:

@@ -24,7 +24,7 @@ EXPORTS = (
     "evogp_select_strategy", "evogp_check_device_flags", "evogp_status_string", "evogp_last_error",
     "evogp_last_launch_count", "evogp_set_kernel_timing", "evogp_classification_accuracy",
     "evogp_eval_paired", "evogp_generate", "evogp_subtree_exchange", "evogp_tournament", "evogp_reproduce",
-    "evogp_tensorize_device",
+    "evogp_tensorize_device", "evogp_set_tuning",
 )
 
 
@@ -74,4 +74,12 @@ def load() -> ctypes.CDLL:
     lib.evogp_last_launch_count.restype = ctypes.c_int32
     lib.evogp_set_kernel_timing.argtypes = [vp, vp]
     lib.evogp_set_kernel_timing.restype = ctypes.c_int
+    lib.evogp_set_tuning.argtypes = [vp]
+    lib.evogp_set_tuning.restype = ctypes.c_int
     return lib
+
+
+class Tuning(ctypes.Structure):
+    """evogp_tuning (include/evogp.h): launch-plan overrides, 0 = default."""
+    _fields_ = [("target_warps", ctypes.c_int32), ("no_reorder", ctypes.c_int32), ("no_fuse", ctypes.c_int32),
+                ("K", ctypes.c_int32)]

@@ -15,6 +15,7 @@ thread_local char t_last_error[512] = "no error";
 thread_local int32_t t_last_launches = 0;
 thread_local void* t_ev_start = nullptr;
 thread_local void* t_ev_end = nullptr;
+thread_local evogp_tuning t_tuning = {0, 0, 0, 0};
 
 int current_device() {
   int dev = 0;
@@ -89,6 +90,8 @@ int run(int mode, const int16_t* type, const float* value, const int16_t* size, 
 }
 
 }  // namespace
+
+const evogp_tuning& tuning() { return t_tuning; }
 
 void set_last_error(const char* msg) {
   std::strncpy(t_last_error, msg, sizeof(t_last_error) - 1);
@@ -231,5 +234,15 @@ extern "C" int evogp_set_kernel_timing(void* start_event, void* end_event) {
   if ((start_event == nullptr) != (end_event == nullptr)) return fail(EVOGP_E_ARG, "need both events or neither");
   t_ev_start = start_event;
   t_ev_end = end_event;
+  return EVOGP_OK;
+}
+
+extern "C" int evogp_set_tuning(const evogp_tuning* t) {
+  if (!t) {
+    t_tuning = evogp_tuning{0, 0, 0, 0};
+    return EVOGP_OK;
+  }
+  if (t->target_warps < 0 || t->target_warps > 64) return fail(EVOGP_E_ARG, "target_warps out of range");
+  t_tuning = *t;
   return EVOGP_OK;
 }

@@ -1,0 +1,471 @@
+// compile.cu — a2 + a4: k_prepare, the compile pass that runs before every
+// evaluation kernel (dataset staging, per-row decode / validation,
+// Sethi-Ullman reordering and leaf fusion into program rows).
+#include <algorithm>
+
+#include "interp.cuh"
+
+namespace evogp {
+// ------------------------------------------------------------------------
+// Evaluation-order optimisation (Sethi-Ullman) of a single-output program.
+// For each binary node evaluate first the child whose subtree needs the
+// deeper stack; every operation still sees exactly the same operand values,
+// so results are unchanged (only independent subtrees are reordered) — a
+// swapped node's opcode becomes f_R(a, b) = f(b, a). Stack need with the top
+// of stack in a register: leaf 1; unary = child; binary evaluated B then A:
+// max(need B, need A + 1). Lane 0 computes sizes / needs / swaps in a reverse
+// scan and the new prefix positions in a forward scan; the warp scatters.
+// Multi-output rows are never reordered (Modi sums are order-sensitive).
+// Returns the program's new maximum stack depth.
+// ------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t reversed_op(uint32_t op) {
+  // branch-free (lanes of the compile pass hold different ops): SUB <-> SUB_R,
+  // DIV <-> DIV_R, POW <-> POW_R, LT <-> GT, LE <-> GE; ADD, MUL, MAX, MIN are
+  // symmetric and keep their code
+  const uint32_t f = op - OP_FN;
+  uint32_t r = f;
+  r = f == F_SUB ? F_SUB_R : r;
+  r = f == F_SUB_R ? F_SUB : r;
+  r = f == F_DIV ? F_DIV_R : r;
+  r = f == F_DIV_R ? F_DIV : r;
+  r = f == F_POW ? F_POW_R : r;
+  r = f == F_POW_R ? F_POW : r;
+  r = (f >= F_LT && f <= F_GE) ? (((f - F_LT) ^ 1u) + F_LT) : r;
+  return OP_FN + r;
+}
+
+__device__ int reorder_program(const Node* s_nodes, int n, Node* row, unsigned char* scr, int L, int lane) {  // row: shared or global
+  uint16_t* sz = reinterpret_cast<uint16_t*>(scr);  // subtree size
+  uint16_t* nd = sz + L;                            // stack need
+  uint16_t* np = nd + L;                            // new prefix position
+  uint16_t* st = np + L;                            // scan stack of subtree roots
+  uint8_t* sw = reinterpret_cast<uint8_t*>(st + L); // children swapped
+  int depth = 0;
+  if (lane == 0) {
+    int top = 0;
+    for (int i = n - 1; i >= 0; --i) {
+      const uint32_t op = s_nodes[i + 1].w0 & 0xFFu;
+      const int ar = op <= OP_VAR ? 0 : func_arity(static_cast<int>(op) - OP_FN);
+      int s, q, swp = 0;
+      if (ar == 0) {
+        s = 1;
+        q = 1;
+      } else if (ar == 1) {
+        const int c = st[--top];
+        s = 1 + sz[c];
+        q = nd[c];
+      } else if (ar == 2) {
+        const int a = st[--top], b = st[--top];  // first pop = leftmost child
+        s = 1 + sz[a] + sz[b];
+        const int q_def = max(static_cast<int>(nd[b]), nd[a] + 1);  // B first (prefix order)
+        const int q_swp = max(static_cast<int>(nd[a]), nd[b] + 1);  // A first
+        swp = q_swp < q_def;
+        q = swp ? q_swp : q_def;
+      } else {
+        const int a = st[--top], b = st[--top], c = st[--top];
+        s = 1 + sz[a] + sz[b] + sz[c];
+        q = max(static_cast<int>(nd[c]), max(nd[b] + 1, nd[a] + 2));
+      }
+      sz[i] = static_cast<uint16_t>(s);
+      nd[i] = static_cast<uint16_t>(q);
+      sw[i] = static_cast<uint8_t>(swp);
+      st[top++] = static_cast<uint16_t>(i);
+    }
+    depth = nd[0];
+    np[0] = 0;
+    for (int i = 0; i < n; ++i) {  // parents precede children in prefix order
+      const uint32_t op = s_nodes[i + 1].w0 & 0xFFu;
+      if (op <= OP_VAR) continue;
+      const int ar = func_arity(static_cast<int>(op) - OP_FN);
+      const int c1 = i + 1;
+      if (ar == 1) {
+        np[c1] = np[i] + 1;
+      } else if (ar == 2) {
+        const int c2 = c1 + sz[c1];
+        if (sw[i]) {
+          np[c2] = np[i] + 1;
+          np[c1] = np[c2] + sz[c2];
+        } else {
+          np[c1] = np[i] + 1;
+          np[c2] = np[c1] + sz[c1];
+        }
+      } else {
+        const int c2 = c1 + sz[c1], c3 = c2 + sz[c2];
+        np[c1] = np[i] + 1;
+        np[c2] = np[c1] + sz[c1];
+        np[c3] = np[c2] + sz[c2];
+      }
+    }
+  }
+  __syncwarp();
+  depth = __shfl_sync(FULL_MASK, depth, 0);
+  for (int i = lane; i < n; i += 32) {
+    Node x = s_nodes[i + 1];
+    if (sw[i]) x.w0 = (x.w0 & ~0xFFu) | reversed_op(x.w0 & 0xFFu);
+    row[np[i] + 1] = x;
+  }
+  if (lane == 0) row[0] = s_nodes[0];
+  __syncwarp();
+  return depth;
+}
+
+// Warp-parallel Sethi-Ullman reordering + leaf fusion of a single-output
+// row, written straight into its program row (same decisions as
+// reorder_program followed by fuse_copy). Used when the caller's subtree
+// sizes are consistent — always the case for rows made by evogp_tensorize /
+// evogp_reproduce; checked here in parallel: a leaf has size 1 and walking a
+// node's children by their sizes ends exactly at i + size[i] (by induction
+// from the last node this makes every size the true one). Lanes own 32
+// consecutive nodes:
+//  * needs bottom-up, chunks from the last to the first: in-chunk children
+//    are read by shuffles, iterating until every node is known (children in
+//    later chunks are final, in shared memory);
+//  * new positions top-down: np[j] = j + acc[j], acc[j] = acc[parent] +
+//    (parent swapped ? (j first child ? +size(second) : -size(first)) : 0):
+//    pointer jumping over in-chunk parents by shuffles (5 rounds), chunks
+//    from the first;
+//  * fusion: a unary / binary node absorbs its first-visited child when that
+//    is a leaf that is not the last node; positions are compacted by a
+//    prefix count of the absorbed leaves over new positions;
+//  * scatter of the final words to the global row.
+// Returns the new length (and *depth_out), or -1 when the sizes are
+// inconsistent. Scratch after the decoded nodes: 10 L bytes.
+__device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __restrict__ urow_size, Node* row,
+                                unsigned char* scr, int L, int lane, int* depth_out, bool reorder) {
+  uint16_t* sz = reinterpret_cast<uint16_t*>(scr);
+  uint16_t* nd = sz + L;  // needs; later the absorbed-prefix counts by new position
+  uint16_t* par = nd + L;
+  int16_t* acc = reinterpret_cast<int16_t*>(par + L);
+  uint8_t* sw = reinterpret_cast<uint8_t*>(acc + L);
+  uint8_t* absd = sw + L;  // an absorbed leaf sits at new position q
+  for (int i = lane; i < n; i += 32) {
+    const int v = __ldg(urow_size + i);
+    sz[i] = static_cast<uint16_t>(v < 1 || v > n - i ? 0 : v);
+    sw[i] = 0;
+    absd[i] = 0;
+  }
+  __syncwarp();
+  bool ok = true;
+  for (int i = lane; i < n; i += 32) {
+    const uint32_t op = s_nodes[i + 1].w0 & 0xFFu;
+    const int ar = op <= OP_VAR ? 0 : func_arity(static_cast<int>(op) - OP_FN);
+    const int si = sz[i];
+    int c = i + 1, q = 0;
+    for (; q < ar && c < n; ++q) {
+      par[c] = static_cast<uint16_t>(i);
+      const int sc = sz[c];
+      c = sc ? c + sc : n + 1;
+    }
+    ok = ok && si != 0 && (ar == 0 ? si == 1 : (q == ar && c == i + si));
+  }
+  if (!__all_sync(FULL_MASK, ok) || sz[0] != n) return -1;
+  __syncwarp();
+  const int nblk = (n + 31) >> 5;
+  if (!reorder) {  // fusion only: identity positions
+    for (int j = lane; j < n; j += 32) acc[j] = 0;
+    __syncwarp();
+  } else {
+  // ---- bottom-up needs
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int base = b * 32, i = base + lane;
+    int ar = 0, q = 1, l1 = lane, l2 = lane, l3 = lane, v1 = 1, v2 = 1, v3 = 1;
+    if (i < n) {
+      const uint32_t op = s_nodes[i + 1].w0 & 0xFFu;
+      ar = op <= OP_VAR ? 0 : func_arity(static_cast<int>(op) - OP_FN);
+      q = ar == 0 ? 1 : 0;
+      if (ar >= 1) {
+        const int c1 = i + 1;
+        if (c1 < base + 32) l1 = c1 - base, v1 = 0;
+        else v1 = nd[c1];
+        if (ar >= 2) {
+          const int c2 = c1 + sz[c1];
+          if (c2 < base + 32) l2 = c2 - base, v2 = 0;
+          else v2 = nd[c2];
+          if (ar == 3) {
+            const int c3 = c2 + sz[c2];
+            if (c3 < base + 32) l3 = c3 - base, v3 = 0;
+            else v3 = nd[c3];
+          }
+        }
+      }
+    }
+    // branch-free iterations (selects only: no divergence bookkeeping)
+    uint8_t swp = 0;
+    while (!__all_sync(FULL_MASK, q != 0)) {
+      const int x1 = __shfl_sync(FULL_MASK, q, l1);
+      const int x2 = __shfl_sync(FULL_MASK, q, l2);
+      const int x3 = __shfl_sync(FULL_MASK, q, l3);
+      const int n1 = v1 ? v1 : x1, n2 = v2 ? v2 : x2, n3 = v3 ? v3 : x3;
+      const int q_def = max(n2, n1 + 1), q_swp = max(n1, n2 + 1);
+      const int q_new = ar == 1 ? n1 : (ar == 2 ? min(q_def, q_swp) : max(n3, max(n2 + 1, n1 + 2)));
+      const bool now = q == 0 && n1 != 0 && n2 != 0 && n3 != 0;
+      swp = (now && ar == 2) ? static_cast<uint8_t>(q_swp < q_def) : swp;
+      q = now ? q_new : q;
+    }
+    if (i < n) {
+      nd[i] = static_cast<uint16_t>(q);
+      sw[i] = swp;
+    }
+    __syncwarp();
+  }
+  *depth_out = nd[0];
+  // ---- top-down positions (pointer jumping inside a chunk)
+  for (int b = 0; b < nblk; ++b) {
+    const int base = b * 32, j = base + lane;
+    int a = 0, ptr = -1;
+    if (j < n && j > 0) {
+      const int pj = par[j];
+      int off = 0;
+      if (sw[pj]) {
+        const int f = pj + 1;
+        off = j == f ? static_cast<int>(sz[f + sz[f]]) : -static_cast<int>(sz[f]);
+      }
+      if (pj < base) {
+        a = acc[pj] + off;
+      } else {
+        a = off;
+        ptr = pj - base;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      const int src = ptr >= 0 ? ptr : lane;
+      const int ap = __shfl_sync(FULL_MASK, a, src);
+      const int pp = __shfl_sync(FULL_MASK, ptr, src);
+      if (ptr >= 0) {
+        a += ap;
+        ptr = pp;
+      }
+    }
+    if (j < n) acc[j] = static_cast<int16_t>(a);
+    __syncwarp();
+  }
+  }
+  // ---- fusion decisions (sw bit 1: absorbs its first-visited child, bit 2:
+  // its second-visited child); absorbed leaves marked at their new positions.
+  // A node absorbs its first-visited child when that is a leaf; a binary node
+  // whose first-visited child is not a leaf absorbs its second-visited child
+  // when that is a leaf (operand b is then the leaf, under the unreversed
+  // op: g(F1, leaf)). The last node is never absorbed (it starts the stack).
+  for (int j = lane; j < n; j += 32) {
+    const uint32_t op = s_nodes[j + 1].w0 & 0xFFu;
+    if (op <= OP_VAR) continue;
+    const int ar = func_arity(static_cast<int>(op) - OP_FN);
+    if (ar > 2) continue;
+    const int c1 = j + 1;
+    const bool swp = ar == 2 && (sw[j] & 1);
+    const int f1 = swp ? c1 + sz[c1] : c1;
+    const int pos1 = f1 + acc[f1];
+    if ((s_nodes[f1 + 1].w0 & 0xFFu) <= OP_VAR) {
+      if (pos1 != n - 1) {
+        absd[pos1] = 1;
+        sw[j] |= 2;
+      }
+      continue;
+    }
+    if (ar == 2) {
+      const int f2 = swp ? c1 : c1 + sz[c1];
+      const int pos2 = f2 + acc[f2];
+      if ((s_nodes[f2 + 1].w0 & 0xFFu) <= OP_VAR && pos2 != n - 1) {
+        absd[pos2] = 1;
+        sw[j] |= 4;
+      }
+    }
+  }
+  __syncwarp();
+  // exclusive prefix count of the absorbed positions -> nd[q]
+  int carry = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int q = base + lane;
+    const bool f = q < n && absd[q];
+    const unsigned m = __ballot_sync(FULL_MASK, f);
+    if (q < n) nd[q] = static_cast<uint16_t>(carry + __popc(m & ((1u << lane) - 1u)));
+    carry += __popc(m);
+  }
+  __syncwarp();
+  // ---- scatter the final words
+  for (int j = lane; j < n; j += 32) {
+    const int pos = j + acc[j];
+    if (absd[pos]) continue;  // an absorbed leaf
+    Node x = s_nodes[j + 1];
+    const uint32_t op = x.w0 & 0xFFu;
+    if (op > OP_VAR) {
+      const int ar = func_arity(static_cast<int>(op) - OP_FN);
+      const uint8_t fl = sw[j];
+      const bool swp = ar == 2 && (fl & 1);
+      uint32_t g = swp ? reversed_op(op) : op;
+      if (ar <= 2 && (fl & 6)) {
+        const int c1 = j + 1;
+        const int c2 = ar == 2 ? c1 + sz[c1] : c1;
+        // first-visited absorbed: f(leaf, top) as f_R(top, leaf) (unary keeps
+        // its op); second-visited absorbed: g(top, leaf) as is
+        const int leaf = (fl & 2) ? (swp ? c2 : c1) : (swp ? c1 : c2);
+        if ((fl & 2) && ar == 2) g = reversed_op(g);
+        const Node l = s_nodes[leaf + 1];
+        x.w0 = (x.w0 & ~0xFFu) | g | kFuse | ((l.w0 & 0xFFu) == OP_VAR ? kFuseVar : 0u);
+        x.w1 = l.w1;
+      } else {
+        x.w0 = (x.w0 & ~0xFFu) | g;
+      }
+    }
+    row[pos - nd[pos] + 1] = x;
+  }
+  if (lane == 0) row[0] = s_nodes[0];
+  __syncwarp();
+  return n - carry;
+}
+
+// Leaf fusion: a unary/binary node whose first child (the next node in
+// prefix order) is a leaf absorbs that leaf — its payload moves into w1 and
+// the flags kFuse / kFuseVar are set. The interpreter then computes a binary
+// f(leaf, top) as f_R(top, leaf) (the leaf is operand b: no push, no pop) and
+// a unary f(leaf) by pushing the old top and applying f to the leaf: the same
+// operations on the same operands, one dispatch fewer per absorbed leaf. The
+// last node (the first one evaluated) is never absorbed. Warp-parallel:
+// decisions are local, positions come from a ballot prefix count.
+__device__ int fuse_copy(const Node* prog, int n, Node* row, int lane) {
+  int carry = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    bool keep = false;
+    Node y{0u, 0u};
+    if (i < n) {
+      y = prog[i + 1];
+      const uint32_t op = y.w0 & 0xFFu;
+      const bool absorbed = op <= OP_VAR && i >= 1 && i != n - 1 && (prog[i].w0 & 0xFFu) >= OP_FN &&
+                            func_arity(static_cast<int>(prog[i].w0 & 0xFFu) - OP_FN) <= 2;
+      keep = !absorbed;
+      if (keep && op >= OP_FN && i + 1 < n - 1) {
+        const int ar = func_arity(static_cast<int>(op) - OP_FN);
+        const Node leaf = prog[i + 2];
+        const uint32_t lop = leaf.w0 & 0xFFu;
+        if (ar <= 2 && lop <= OP_VAR) {
+          const uint32_t fop = ar == 2 ? reversed_op(op) : op;
+          y.w0 = (y.w0 & ~0xFFu) | fop | kFuse | (lop == OP_VAR ? kFuseVar : 0u);
+          y.w1 = leaf.w1;
+        }
+      }
+    }
+    const unsigned m = __ballot_sync(FULL_MASK, keep);
+    if (keep) row[carry + __popc(m & ((1u << lane) - 1u)) + 1] = y;
+    carry += __popc(m);
+  }
+  if (lane == 0) row[0] = prog[0];
+  __syncwarp();
+  return carry;
+}
+
+// ------------------------------------------------------------------------
+// a2 + a4 (compile): one launch before the evaluation kernel
+//   * X (row-major or SoA) -> padded SoA rows Xs[n_in][Dpad] (+ y for the SSE)
+//   * every tree row -> its decoded program row (one warp per tree): decode,
+//     validate, stack depth; so the evaluation kernels only copy programs
+//   * clears the per-tree completion counters and the work-queue tickets
+// ------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* __restrict__ X, int32_t x_layout,
+                                                 const float* __restrict__ y, int y_is_label, int64_t n_counters) {
+  const int64_t rows = p.n_in + (y ? 1 : 0);
+  const int64_t total = rows * p.Dpad;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  float* xs = const_cast<float*>(p.xs);
+  for (int64_t e = t0; e < total; e += stride) {
+    const int64_t k = e / p.Dpad, d = e - k * p.Dpad;
+    float v = 0.f;
+    if (d < p.D) {
+      if (k == p.n_in) v = y_is_label ? static_cast<float>(reinterpret_cast<const int32_t*>(y)[d]) : y[d];
+      else v = x_layout == EVOGP_X_SOA ? X[k * p.D + d] : X[d * p.n_in + k];
+    }
+    xs[e] = v;
+  }
+  for (int64_t e = t0; e < n_counters; e += stride) p.counters[e] = 0;
+  // the deep-pool locks are re-zeroed every call: a workspace may be reused
+  // across plans whose section offsets differ (e.g. inter vs intra partials)
+  for (int64_t e = t0; e < p.deep_slots; e += stride) p.deep_locks[e] = 0;
+  if (t0 == 0) {
+    p.ctl->work = 0;
+    p.ctl->deep = 0;
+    p.ctl->cold_chunks = 0;
+  }
+  // compile: warp per tree
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = stride >> 5;
+  extern __shared__ __align__(16) unsigned char smem[];
+  unsigned char* scratch = smem + static_cast<size_t>(threadIdx.x >> 5) * p.reorder_scratch_bytes;
+  for (int64_t tp = t0 >> 5; tp < p.P; tp += nwarps) {
+    Node* row = p.prog + tp * p.prog_ld;
+    TreeInfo ti;
+    if (p.reorder_scratch_bytes > 0) {
+      // decode into shared scratch; reorder when the row is deeper than the
+      // evaluation kernel's shared stack; then fuse leaves while copying out
+      Node* s_nodes = reinterpret_cast<Node*>(scratch);
+      Node* s_reord = s_nodes + (p.L + 1);
+      ti = stage_tree_warp(p, tp, s_nodes, lane);
+      const Node* prog = s_nodes;
+      if (ti.valid && p.fuse && ti.maxdepth - 1 > p.reorder_above) {
+        // warp-parallel reorder + fusion straight into the program row; rows
+        // with inconsistent caller sizes take fuse_copy (no reordering). Rows
+        // that need no reordering also take fuse_copy: the second-child fusion
+        // of reorder_fuse_par(reorder = false) measured +1-2% in the kernels
+        // but -5% on c4's whole step (the compile pass costs more than it saves)
+        int dep = ti.maxdepth;
+        const int len = reorder_fuse_par(s_nodes, ti.len, p.size + tp * p.ld, row, scratch + (p.L + 1) * 8, p.L,
+                                         lane, &dep, true);
+        if (len > 0) {
+          ti.len = len;
+          ti.maxdepth = dep;
+          goto compiled;
+        }
+      } else if (ti.valid && ti.maxdepth - 1 > p.reorder_above) {
+        {
+          ti.maxdepth = reorder_program(s_nodes, ti.len, s_reord, scratch + 2 * (p.L + 1) * 8, p.L, lane);
+          prog = s_reord;
+        }
+      }
+      if (ti.valid && p.fuse) {
+        ti.len = fuse_copy(prog, ti.len, row, lane);
+      } else {
+        const uint2* src = reinterpret_cast<const uint2*>(prog);
+        for (int i = lane; i <= ti.len; i += 32) reinterpret_cast<uint2*>(row)[i] = src[i];
+        __syncwarp();
+      }
+    } else {
+      ti = stage_tree_warp(p, tp, row, lane);
+    }
+  compiled:
+    if (lane == 0) {
+      p.info[tp] = TreeMeta{ti.len, ti.valid ? (ti.maxdepth | (ti.paper ? kPaperRow : 0)) : -1};
+      if (!ti.valid) atomicOr(&p.ctl->flags, 1);
+    }
+    __syncwarp();
+  }
+}
+
+// Host launcher of k_prepare: one warp per tree (up to 8 per CTA, fewer when
+// the compile scratch is large), grid-stride over the staged dataset too.
+void launch_prepare(const KParams& kp, int mode, const float* X, int32_t x_layout, const float* y,
+                    cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(kp.n_in + 1) * kp.Dpad;
+  // warps per CTA such that their compile scratch fits the opt-in shared memory
+  constexpr int wpb_cap = 8;
+  const int wpb = kp.reorder_scratch_bytes > 0 ? std::max(1, std::min(wpb_cap, (220 * 1024) / kp.reorder_scratch_bytes))
+                                               : wpb_cap;
+  const int threads = 32 * wpb;
+  const size_t psmem = static_cast<size_t>(wpb) * kp.reorder_scratch_bytes;
+  if (psmem > 48 * 1024) {
+    static thread_local int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+      cudaFuncSetAttribute(k_prepare, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      attr_dev = dev;
+    }
+  }
+  const int64_t blocks = std::max<int64_t>(
+      1, std::min<int64_t>(std::max((total + threads - 1) / threads, (kp.P + wpb - 1) / wpb),
+                           static_cast<int64_t>(kp.sms) * 16 * (8 / wpb)));
+  k_prepare<<<static_cast<int>(blocks), threads, psmem, s>>>(kp, X, x_layout, mode_reduce(mode) ? y : nullptr,
+                                                            mode == MODE_CLS, mode_reduce(mode) ? kp.P : 0);
+}
+
+}  // namespace evogp

@@ -1,0 +1,15 @@
+// eval_intra_k4.cu — kernel (b) instantiations at K = 4, multi-output (Modi)
+// modes: the Modi store and the classification epilogue.
+#include "interp.cuh"
+
+namespace evogp {
+
+const void* kernel_intra_k4(int mode) {
+  switch (mode) {
+    case MODE_EVALN: return reinterpret_cast<const void*>(&k_intra<4, MODE_EVALN>);
+    case MODE_CLS: return reinterpret_cast<const void*>(&k_intra<4, MODE_CLS>);
+  }
+  return nullptr;
+}
+
+}  // namespace evogp

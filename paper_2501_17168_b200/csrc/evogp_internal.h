@@ -4,6 +4,8 @@
 #include <cstddef>
 #include <cstdint>
 
+#include <cuda_runtime.h>
+
 #include "../../include/evogp.h"
 
 #ifdef __CUDACC__
@@ -60,6 +62,10 @@ struct alignas(8) Node {
   uint32_t w1;
 };
 
+// warps per CTA of kernel (a) and kernel (b)
+constexpr int kInterWarps = 4;
+constexpr int kIntraWarps = 8;
+
 enum Mode : int { MODE_EVAL1 = 0, MODE_EVALN = 1, MODE_SSE = 2, MODE_CLS = 3 };
 // Modes whose trees accumulate Modi outputs, and modes reduced to one number per tree
 EVOGP_HD constexpr bool mode_multi(int m) { return m == MODE_EVALN || m == MODE_CLS; }
@@ -85,6 +91,7 @@ struct KParams {
   const int16_t* type;
   const float* value;
   const int16_t* size;
+  int32_t sms;  // SMs of the device the plan was made for
   int64_t P;
   int32_t L;   // max_len
   int32_t ld;  // row stride
@@ -142,6 +149,21 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
 int launch(Plan& pl, int mode, const float* X, int32_t x_layout, const float* y, void* stream, int* n_launches,
            void* ev_start = nullptr, void* ev_end = nullptr);
 int select_strategy(int64_t P, int64_t D, int32_t L, int32_t n_out, int device);
+// the calling thread's tuning (evogp_set_tuning; defaults when never set)
+const evogp_tuning& tuning();
+
+// compile.cu
+void launch_prepare(const KParams& kp, int mode, const float* X, int32_t x_layout, const float* y,
+                    cudaStream_t s);
+
+// eval_*.cu: the instantiated evaluation kernels for one (strategy, K), by mode
+// (nullptr for a mode that is not instantiated)
+const void* kernel_inter_k1(int mode);
+const void* kernel_inter_k2(int mode);
+const void* kernel_inter_k4(int mode);
+const void* kernel_inter_k8(int mode);
+const void* kernel_intra_k4(int mode);
+const void* kernel_intra_k8(int mode);
 
 // paired.cu
 int launch_paired(const int16_t* type, const float* value, const int16_t* size, int64_t P, int32_t L, int32_t ld,

@@ -18,6 +18,8 @@ from __future__ import annotations
 
 import ctypes
 
+import numpy as np
+
 from ._lib import OK
 
 
@@ -58,6 +60,10 @@ class HostSRFitness:
             e.record(self.s_comp)
         self.k = 0  # chunk buffer-set counter, continued across calls
         self.kc = 0  # call counter (dataset buffer set)
+        self.nodes_max = int(nodes_max)
+        # pinned staging of chunk-relative offsets (a chunk whose first node is
+        # not node 0 is rebased on the host before its copy), per buffer set
+        self.h_off = [torch.empty(pc + 1, dtype=torch.int64).pin_memory() for _ in range(2)]
 
     def __call__(self, offsets, types, values, out, X=None, y=None):
         """offsets/types/values: pinned host torch tensors (CSR); out: pinned
@@ -77,7 +83,14 @@ class HostSRFitness:
 
         P = int(offsets.numel()) - 1
         off_np = offsets.numpy()
+        if P > self.chunks * self.pc:
+            raise ValueError(f"population of {P} trees exceeds this pipeline's capacity {self.chunks * self.pc}")
         bounds = [min(P, c * self.pc) for c in range(self.chunks + 1)]
+        for c in range(self.chunks):
+            p0, p1 = bounds[c], bounds[c + 1]
+            if p1 > p0 and int(off_np[p1]) - int(off_np[p0]) > self.nodes_max:
+                raise ValueError(f"chunk {c} holds {int(off_np[p1]) - int(off_np[p0])} nodes > nodes_max "
+                                 f"{self.nodes_max}")
         if X is not None and self.Xs is None:
             self.Xs = [torch.empty_like(self.X) for _ in range(2)]
             self.ys = [torch.empty_like(self.y) for _ in range(2)]
@@ -98,21 +111,27 @@ class HostSRFitness:
             b = self.k & 1
             self.k += 1
             n0, n1 = int(off_np[p0]), int(off_np[p1])
+            if n0 != 0:
+                # chunk-relative offsets: the previous copy out of this staging
+                # buffer (same buffer set) must have finished before rewriting it
+                self.ev_h2d[b].synchronize()
+                ho = self.h_off[b][: p1 - p0 + 1]
+                np.subtract(off_np[p0: p1 + 1], n0, out=ho.numpy())
+                src_off = ho
+            else:
+                src_off = offsets[p0: p1 + 1]
             with torch.cuda.stream(self.s_copy):
                 self.s_copy.wait_event(self.ev_free[b])
-                self.d_off[b][: p1 - p0 + 1].copy_(offsets[p0: p1 + 1], non_blocking=True)
+                self.d_off[b][: p1 - p0 + 1].copy_(src_off, non_blocking=True)
                 self.d_ty[b][: n1 - n0].copy_(types[n0:n1], non_blocking=True)
                 self.d_va[b][: n1 - n0].copy_(values[n0:n1], non_blocking=True)
                 self.ev_h2d[b].record(self.s_copy)
             with torch.cuda.stream(self.s_comp):
                 self.s_comp.wait_event(self.ev_h2d[b])
                 t, v, s = (r[: p1 - p0] for r in self.rows[b])
-                # the chunk's offsets are global node indices: pass node arrays
-                # based n0 elements before the copied slice (never dereferenced there)
                 st = _LIB.evogp_tensorize_device(
-                    p1 - p0, ctypes.c_void_p(self.d_off[b].data_ptr()),
-                    ctypes.c_void_p(self.d_ty[b].data_ptr() - 2 * n0),
-                    ctypes.c_void_p(self.d_va[b].data_ptr() - 4 * n0), self.L, self.n_in, 1,
+                    p1 - p0, ctypes.c_void_p(self.d_off[b].data_ptr()), ctypes.c_void_p(self.d_ty[b].data_ptr()),
+                    ctypes.c_void_p(self.d_va[b].data_ptr()), self.L, self.n_in, 1,
                     ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(s.data_ptr()),
                     ctypes.c_void_p(0), ctypes.c_void_p(self.s_comp.cuda_stream))
                 if st != OK:
