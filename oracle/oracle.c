@@ -327,8 +327,13 @@ static double cert_f(int f, const double* a, const double* e, double r, int* rob
   }
   /* rounding of the result itself, plus an absolute floor for underflow */
   out += ulp_budget(f) * TWO_M23 * fabs(r) + FP32_TINY;
-  /* sin/cos on the GPU are the SFU approximations after a 2*pi reduction:
-   * absolute error <= 2^-20 (measured max 2^-20.6 on B200; R14) */
+  /* sin/cos on the GPU are the SFU approximations (sin.approx / cos.approx,
+   * i.e. CUDA's __sinf / __cosf) after a Cody-Waite 2*pi reduction. The CUDA
+   * C++ Programming Guide's intrinsic-function table bounds __sinf / __cosf
+   * on [-pi, pi] by 2^-21.41 / 2^-21.19 absolute; an exhaustive B200 sweep of
+   * every FP32 argument in [-pi, pi] measured 2^-21.46 / 2^-21.24
+   * (tests/test_gpu_accuracy.py). The budget 2^-20 adds room for the
+   * reduction's own error at |x| up to 105615 (R14). */
   if (f == F_SIN || f == F_COS) out += SFU_TRIG_ABS;
   if (isnan(out)) out = INFINITY;
   return out;

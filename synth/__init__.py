@@ -29,8 +29,7 @@ M_PAPER = (0, 1, 2, 3, 4, 5, 6)
 M_FULL = tuple(range(22))
 M_BOUNDED = (0, 1, 2, 3, 7, 8, 4, 5, 12)
 M_IEEE = (0, 1, 2, 3, 15, 13, 14, 7, 8, 17, 18, 19, 20, 21)
-M_ARITH = (0, 1, 2, 3)  # the paper set's IEEE-exact part {+, -, *, /}: pins the paper-set interpreter copy
-MIXES = {"paper": M_PAPER, "full": M_FULL, "bounded": M_BOUNDED, "ieee": M_IEEE, "arith": M_ARITH}
+MIXES = {"paper": M_PAPER, "full": M_FULL, "bounded": M_BOUNDED, "ieee": M_IEEE}
 
 
 def build(force: bool = False) -> str:
