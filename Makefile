@@ -11,7 +11,7 @@ CU := eval_inter_k8 eval_inter_k4 eval_inter_k2 eval_inter_k1 eval_intra_k8 eval
       paired variation tensorize_dev capi
 OBJDIR := build/obj
 OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU))) $(OBJDIR)/tensorize.o
-HDRS := $(CSRC)/evogp_internal.h $(CSRC)/fastmath.cuh $(CSRC)/decode.cuh $(CSRC)/interp.cuh \
+HDRS := $(CSRC)/evogp_internal.h $(CSRC)/fastmath.cuh $(CSRC)/decode.cuh $(CSRC)/interp.cuh $(CSRC)/hot.cuh $(CSRC)/hot_ptx.inc \
         $(CSRC)/selector_table.inc include/evogp.h
 
 all: $(LIB) oracle/liboracle.so synth/libsynth.so

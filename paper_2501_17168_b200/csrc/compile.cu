@@ -308,7 +308,7 @@ __device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __res
         x.w0 = (x.w0 & ~0xFFu) | g;
       }
     }
-    row[pos - nd[pos] + 1] = x;
+    row[pos - nd[pos] + 1] = finalize_hot(x);
   }
   if (lane == 0) row[0] = s_nodes[0];
   __syncwarp();
@@ -347,7 +347,7 @@ __device__ int fuse_copy(const Node* prog, int n, Node* row, int lane) {
       }
     }
     const unsigned m = __ballot_sync(FULL_MASK, keep);
-    if (keep) row[carry + __popc(m & ((1u << lane) - 1u)) + 1] = y;
+    if (keep) row[carry + __popc(m & ((1u << lane) - 1u)) + 1] = finalize_hot(y);
     carry += __popc(m);
   }
   if (lane == 0) row[0] = prog[0];
@@ -425,12 +425,14 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
       if (ti.valid && p.fuse) {
         ti.len = fuse_copy(prog, ti.len, row, lane);
       } else {
-        const uint2* src = reinterpret_cast<const uint2*>(prog);
-        for (int i = lane; i <= ti.len; i += 32) reinterpret_cast<uint2*>(row)[i] = src[i];
+        for (int i = lane; i <= ti.len; i += 32) {
+          const Node x = prog[i];
+          row[i] = i == 0 ? x : finalize_hot(x);
+        }
         __syncwarp();
       }
     } else {
-      ti = stage_tree_warp(p, tp, row, lane);
+      ti = stage_tree_warp(p, tp, row, lane, p.n_out == 1);  // single-output rows get hot codes
     }
   compiled:
     if (lane == 0) {

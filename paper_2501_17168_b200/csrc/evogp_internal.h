@@ -57,6 +57,26 @@ constexpr uint32_t kNoSlot = 0xFF;
 // a VAR (w1 = its X offset), else a CONST (w1 = its bits).
 constexpr uint32_t kFuse = 1u << 16;
 constexpr uint32_t kFuseVar = 1u << 17;
+// Hot code (compile pass, single-output programs): w0 bits 24-31 hold a
+// dense opcode for the packed interpreter (hot.cuh) that already encodes the
+// operand source of a fused leaf, so its dispatch is one switch with no flag
+// tests. S = operand b popped from the stack, C = b is a fused CONST leaf
+// (w1 = its bits), V = b is a fused VAR leaf (w1 = its X offset); unary T =
+// the top of the stack, V = push the top, then f(x[w1]). A unary node over a
+// CONST leaf is folded by the compile pass into PUSH_C of its value. Codes
+// 0..kHotPaperEnd-1 cover the paper's set and the reversed SUB/DIV.
+enum HotCode : uint32_t {
+  HC_END = 0, HC_PUSH_C, HC_PUSH_V,
+  HC_ADD = 3, HC_SUB = 6, HC_MUL = 9, HC_DIV = 12, HC_SUBR = 15, HC_DIVR = 18,  // + {S, C, V}
+  HC_SIN = 21, HC_COS = 23, HC_TAN = 25,                                     // + {T, V}
+  HC_PAPER_END = 27,
+  HC_MAX = 27, HC_MIN = 30, HC_POW = 33, HC_POWR = 36, HC_LT = 39, HC_GT = 42, HC_LE = 45, HC_GE = 48,
+  HC_LOG = 51, HC_EXP = 53, HC_TANH = 55, HC_NEG = 57, HC_ABS = 59, HC_SQRT = 61, HC_INV = 63,
+  HC_IF = 65,
+  HC_COUNT = 66
+};
+constexpr uint32_t kHotShift = 24;
+
 struct alignas(8) Node {
   uint32_t w0;
   uint32_t w1;
@@ -65,6 +85,52 @@ struct alignas(8) Node {
 // warps per CTA of kernel (a) and kernel (b)
 constexpr int kInterWarps = 4;
 constexpr int kIntraWarps = 8;
+
+// Hot code of a decoded single-output node word (op in bits 0-7, fuse flags
+// kFuse / kFuseVar). A unary node with a fused CONST leaf has no code here:
+// the compile pass folds it (returns HC_END as a marker).
+EVOGP_HD inline uint32_t hot_code_of(uint32_t w0) {
+  const uint32_t op = w0 & 0xFFu;
+  if (op == OP_CONST) return HC_PUSH_C;
+  if (op == OP_VAR) return HC_PUSH_V;
+  const int f = static_cast<int>(op) - OP_FN;
+  const uint32_t src = (w0 & kFuse) ? ((w0 & kFuseVar) ? 2u : 1u) : 0u;
+  uint32_t base;
+  switch (f) {
+    case F_ADD: base = HC_ADD; break;
+    case F_SUB: base = HC_SUB; break;
+    case F_MUL: base = HC_MUL; break;
+    case F_DIV: base = HC_DIV; break;
+    case F_SUB_R: base = HC_SUBR; break;
+    case F_DIV_R: base = HC_DIVR; break;
+    case F_MAX: base = HC_MAX; break;
+    case F_MIN: base = HC_MIN; break;
+    case F_POW: base = HC_POW; break;
+    case F_POW_R: base = HC_POWR; break;
+    case F_LT: base = HC_LT; break;
+    case F_GT: base = HC_GT; break;
+    case F_LE: base = HC_LE; break;
+    case F_GE: base = HC_GE; break;
+    case F_IF: return HC_IF;
+    default: {  // unary: T or V (a fused CONST operand is folded away)
+      uint32_t u;
+      switch (f) {
+        case F_SIN: u = HC_SIN; break;
+        case F_COS: u = HC_COS; break;
+        case F_TAN: u = HC_TAN; break;
+        case F_LOG: u = HC_LOG; break;
+        case F_EXP: u = HC_EXP; break;
+        case F_TANH: u = HC_TANH; break;
+        case F_NEG: u = HC_NEG; break;
+        case F_ABS: u = HC_ABS; break;
+        case F_SQRT: u = HC_SQRT; break;
+        default: u = HC_INV; break;
+      }
+      return src == 1u ? HC_END : u + (src == 2u ? 1u : 0u);
+    }
+  }
+  return base + src;
+}
 
 enum Mode : int { MODE_EVAL1 = 0, MODE_EVALN = 1, MODE_SSE = 2, MODE_CLS = 3 };
 // Modes whose trees accumulate Modi outputs, and modes reduced to one number per tree

@@ -46,7 +46,10 @@ constexpr int32_t kPaperRow = 1 << 30;
 // after processing node i is the suffix sum d_i = sum_{j>=i} c_j; a row is
 // well-formed iff every d_i >= 1 and d_0 == 1 (P:358 evaluation never
 // underflows and leaves exactly the root).
-__device__ __forceinline__ TreeInfo stage_tree_warp(const KParams& p, int64_t tp, Node* s_tree, int lane) {
+__device__ __forceinline__ Node finalize_hot(Node x);
+
+__device__ __forceinline__ TreeInfo stage_tree_warp(const KParams& p, int64_t tp, Node* s_tree, int lane,
+                                                    bool hot = false) {
   const int16_t* trow = p.type + tp * p.ld;
   const float* vrow = p.value + tp * p.ld;
   const int len0 = __ldg(p.size + tp * p.ld);
@@ -64,7 +67,7 @@ __device__ __forceinline__ TreeInfo stage_tree_warp(const KParams& p, int64_t tp
       const int16_t t = __ldg(trow + i);
       const float v = __ldg(vrow + i);
       ok = decode_node(t, v, p.n_in, p.n_out, p.Dpad, nd, ar) && ok;
-      s_tree[i + 1] = nd;
+      s_tree[i + 1] = hot ? finalize_hot(nd) : nd;
       c = 1 - ar;
       paper = paper && (nd.w0 & 0xFFu) <= OP_FN + F_TAN;
     }
@@ -185,6 +188,56 @@ __device__ __forceinline__ void vld_nc(const float* p, float (&v)[K]) {
 // ------------------------------------------------------------------------
 // protected log (reading R3): |a| > delta ? log|a| : 0
 __device__ __forceinline__ float fn_plog(float a) { return fabsf(a) > kDelta ? logf(fabsf(a)) : 0.0f; }
+
+// element forms shared by the packed interpreter (hot.cuh): the same
+// expressions as interpret's cases (reading R3)
+__device__ __forceinline__ float hot_pow(float a, float b) { return powf(fabsf(a), b); }
+__device__ __forceinline__ float hot_powr(float a, float b) { return powf(fabsf(b), a); }
+__device__ __forceinline__ float hot_lt(float a, float b) { return a < b ? 1.0f : 0.0f; }
+__device__ __forceinline__ float hot_gt(float a, float b) { return a > b ? 1.0f : 0.0f; }
+__device__ __forceinline__ float hot_le(float a, float b) { return a <= b ? 1.0f : 0.0f; }
+__device__ __forceinline__ float hot_ge(float a, float b) { return a >= b ? 1.0f : 0.0f; }
+// fast forms on their checked range (callers bail outside it)
+__device__ __forceinline__ float hot_sqrt(float x) {
+  const float a = fabsf(x);
+  return a == 0.0f ? 0.0f : sqrt_fast(a);
+}
+__device__ __forceinline__ float hot_inv(float a) { return fabsf(a) > kDelta ? rcp_fast(a) : 0.0f; }
+
+// The value a unary function gives a CONST operand c, exactly as the
+// interpreter computes it (fast path on its range, the library function
+// elsewhere: the cold copy's element form, which every copy agrees with).
+// The compile pass folds unary-over-CONST nodes with it.
+static __device__ __noinline__ float fold_unary(int f, float c) {
+  const float a = fabsf(c);
+  switch (f) {
+    case F_SIN: return a <= kTrigReduceMax ? fm_sin_fast(c) : slow_sinf(c);
+    case F_COS: return a <= kTrigReduceMax ? fm_cos_fast(c) : slow_cosf(c);
+    case F_TAN: return a <= kTrigReduceMax ? fm_tan_fast(c) : slow_tanf(c);
+    case F_LOG: return fn_plog(c);
+    case F_EXP: return expf(c);
+    case F_TANH: return tanhf(c);
+    case F_NEG: return -c;
+    case F_ABS: return a;
+    case F_SQRT: return a == 0.0f ? 0.0f : ((a <= kSqrtRange && a >= kSqrtRangeMin) ? sqrt_fast(a) : slow_sqrt(a));
+    default:  // F_INV
+      return a > kDelta ? (a <= kSqrtRange ? rcp_fast(c) : slow_rcp(c)) : 0.0f;
+  }
+}
+
+// Final form of a single-output program word: hot code in bits 24-31; a
+// unary node whose fused operand is a CONST leaf becomes a CONST leaf of
+// its value (the cold copy then pushes the old top and loads it: the same
+// stack effect as the fused unary).
+__device__ __forceinline__ Node finalize_hot(Node x) {
+  const uint32_t op = x.w0 & 0xFFu;
+  if (op >= OP_FN && (x.w0 & kFuse) && !(x.w0 & kFuseVar) && func_arity(static_cast<int>(op) - OP_FN) == 1) {
+    const float v = fold_unary(static_cast<int>(op) - OP_FN, __uint_as_float(x.w1));
+    return Node{OP_CONST | (kNoSlot << 8) | (HC_PUSH_C << kHotShift), __float_as_uint(v)};
+  }
+  x.w0 = (x.w0 & 0x00FFFFFFu) | (hot_code_of(x.w0) << kHotShift);
+  return x;
+}
 
 template <int K, bool MULTI, bool COLD, bool PAPER = false>
 __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len, const float* __restrict__ xl,
@@ -543,6 +596,8 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
   return bail;
 }
 
+#include "hot.cuh"
+
 // ------------------------------------------------------------------------
 // Deep-stack pool: rows whose stack exceeds the shared slots borrow one of
 // `deep_slots` global slots (ticket + per-slot spin lock; holders always
@@ -626,8 +681,15 @@ __device__ __forceinline__ void run_chunk(const KParams& p, const Node* tree, co
   if (MULTI) zero_acc<K>(s_acc_l, p.n_out);
   const int need = ti.maxdepth - 1;  // stack slots below the register top
   if (need <= p.SD) {
-    const bool bail = ti.paper ? interpret<K, MULTI, false, true>(tree, ti.len, xl, s_stack_l, s_acc_l, tos)
-                               : interpret<K, MULTI, false>(tree, ti.len, xl, s_stack_l, s_acc_l, tos);
+    bool bail;
+    if constexpr (!MULTI && K >= 4) {
+      // single-output programs carry hot codes (compile pass): packed interpreter
+      bail = ti.paper ? hot::interp_hot<K, true>(tree, ti.len, xl, s_stack_l, tos)
+                      : hot::interp_hot<K, false>(tree, ti.len, xl, s_stack_l, tos);
+    } else {
+      bail = ti.paper ? interpret<K, MULTI, false, true>(tree, ti.len, xl, s_stack_l, s_acc_l, tos)
+                      : interpret<K, MULTI, false>(tree, ti.len, xl, s_stack_l, s_acc_l, tos);
+    }
     if (__any_sync(FULL_MASK, bail)) {
       if (lane == 0) atomicAdd(&p.ctl->cold_chunks, 1u);
       if (MULTI) {
