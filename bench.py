@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sustain-seconds", type=float, default=1.0)
+    ap.add_argument("--tune", default="", help="evogp_set_tuning overrides, e.g. target_warps=48,no_reorder=1 "
+                                                "(calibration sweeps; results never depend on them)")
     return ap.parse_args()
 
 
@@ -517,6 +519,8 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
 
+    if args.tune:
+        evogp.set_tuning(**{k: int(v) for k, v in (kv.split("=") for kv in args.tune.split(","))})
     axis, (p0, p1), (d0, d1) = local_shards(cfg, rank, world, args.scaling)
     pt = synth.trees(cfg.seed, p0, p1 - p0, cfg.max_len, synth.MIXES[mix], cfg.n_in, cfg.n_out, cfg.modi_prob)
     if cfg.paired:  # NEXT-2: every individual's own B observations, rows p0*B ...

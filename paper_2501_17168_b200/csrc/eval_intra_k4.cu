@@ -1,11 +1,13 @@
 // eval_intra_k4.cu — kernel (b) instantiations at K = 4, multi-output (Modi)
-// modes: the Modi store and the classification epilogue.
+// modes (the Modi store and the classification epilogue) and single-output modes.
 #include "interp.cuh"
 
 namespace evogp {
 
 const void* kernel_intra_k4(int mode) {
   switch (mode) {
+    case MODE_EVAL1: return reinterpret_cast<const void*>(&k_intra<4, MODE_EVAL1>);
+    case MODE_SSE: return reinterpret_cast<const void*>(&k_intra<4, MODE_SSE>);
     case MODE_EVALN: return reinterpret_cast<const void*>(&k_intra<4, MODE_EVALN>);
     case MODE_CLS: return reinterpret_cast<const void*>(&k_intra<4, MODE_CLS>);
   }

@@ -880,7 +880,7 @@ __device__ __forceinline__ long long next_ticket(const KParams& p, int lane) {
 }
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(32 * kInterWarps, 8) k_inter(const KParams p) {
+__global__ void __launch_bounds__(32 * kInterWarps, K >= 16 ? 5 : 8) k_inter(const KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int V = Lay<K>::V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -929,7 +929,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
 }
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(32 * kIntraWarps, 4) k_intra(const KParams p) {
+__global__ void __launch_bounds__(32 * kIntraWarps, K >= 16 ? 2 : 4) k_intra(const KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ double s_red[kIntraWarps];
