@@ -443,6 +443,23 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
   }
 }
 
+// a7 combine: res[t] = (sum over the tree's units of their partials, in unit
+// order) [/ D]. One thread per tree; launched after the evaluation kernel
+// when a tree spans several units.
+__global__ void __launch_bounds__(256) k_combine(const KParams p) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= p.P) return;
+  const double* q = p.partials + t * p.nparts;
+  double acc = 0.0;
+  for (int i = 0; i < p.nparts; ++i) acc += q[i];
+  p.res[t] = p.div_by_D ? acc / static_cast<double>(p.D) : acc;
+}
+
+void launch_combine(const KParams& kp, cudaStream_t s) {
+  const int64_t blocks = (kp.P + 255) / 256;
+  k_combine<<<static_cast<int>(blocks), 256, 0, s>>>(kp);
+}
+
 // Host launcher of k_prepare: one warp per tree (up to 8 per CTA, fewer when
 // the compile scratch is large), grid-stride over the staged dataset too.
 void launch_prepare(const KParams& kp, int mode, const float* X, int32_t x_layout, const float* y,
@@ -467,7 +484,7 @@ void launch_prepare(const KParams& kp, int mode, const float* X, int32_t x_layou
       1, std::min<int64_t>(std::max((total + threads - 1) / threads, (kp.P + wpb - 1) / wpb),
                            static_cast<int64_t>(kp.sms) * 16 * (8 / wpb)));
   k_prepare<<<static_cast<int>(blocks), threads, psmem, s>>>(kp, X, x_layout, mode_reduce(mode) ? y : nullptr,
-                                                            mode == MODE_CLS, mode_reduce(mode) ? kp.P : 0);
+                                                            mode == MODE_CLS, 0);
 }
 
 }  // namespace evogp

@@ -221,6 +221,7 @@ const evogp_tuning& tuning();
 // compile.cu
 void launch_prepare(const KParams& kp, int mode, const float* X, int32_t x_layout, const float* y,
                     cudaStream_t s);
+void launch_combine(const KParams& kp, cudaStream_t s);
 
 // eval_*.cu: the instantiated evaluation kernels for one (strategy, K), by mode
 // (nullptr for a mode that is not instantiated)

@@ -822,32 +822,17 @@ __device__ __forceinline__ double lane_correct(const KParams& p, int64_t chunk_b
   return static_cast<double>(correct);
 }
 
-// Deterministic cross-unit combine of per-tree partial SSEs: every unit
-// writes its partial; the last to arrive (per-tree counter) sums all
-// partials in a fixed order and writes the result (reading R9).
+// Per-tree result of one work unit: the whole tree's value when the tree is
+// one unit, else the unit's partial, summed in a fixed order by k_combine
+// after the kernel (reading R9: deterministic; the kernel boundary orders the
+// partials, so the hot kernel carries no fences or completion counters —
+// an acquire per unit invalidated the SM's L1, measured on c2).
 __device__ __forceinline__ void combine_partial(const KParams& p, int64_t tp, int part, double s, int lane) {
+  if (lane != 0) return;
   if (p.nparts == 1) {
-    if (lane == 0) p.res[tp] = p.div_by_D ? s / static_cast<double>(p.D) : s;
-    return;
-  }
-  int last = 0;
-  if (lane == 0) {
-    __stcg(p.partials + tp * p.nparts + part, s);
-    // release: the partial above is visible before the ticket; acquire: the
-    // last arriver sees every other unit's partial (no full MEMBAR.GPU)
-    int t;
-    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(t) : "l"(p.counters + tp) : "memory");
-    last = (t == p.nparts - 1);
-  }
-  last = __shfl_sync(FULL_MASK, last, 0);
-  if (!last) return;
-  __syncwarp();  // memory ordering: lane 0's acquire happens-before the other lanes' reads
-  double acc = 0.0;
-  for (int q = lane; q < p.nparts; q += 32) acc += __ldcg(p.partials + tp * p.nparts + q);
-  acc = warp_sum_d(acc);  // fixed lane-strided order, then a fixed shuffle tree
-  if (lane == 0) {
-    p.res[tp] = p.div_by_D ? acc / static_cast<double>(p.D) : acc;
-    p.counters[tp] = 0;
+    p.res[tp] = p.div_by_D ? s / static_cast<double>(p.D) : s;
+  } else {
+    p.partials[tp * p.nparts + part] = s;
   }
 }
 
@@ -889,11 +874,14 @@ __global__ void __launch_bounds__(32 * kInterWarps, K >= 16 ? 5 : 8) k_inter(con
   float* s_stack_l = reinterpret_cast<float*>(wbase + p.tree_bytes) + lane * V;
   float* s_acc_l = s_stack_l + p.SD * 32 * K;
   const long long nunits = p.P * p.nch;
-  long long u = next_ticket(p, lane);
+  // first unit: the warp's global index (no atomic); then the shared queue,
+  // whose tickets start after the grid's warps
+  const long long nwarps_grid = static_cast<long long>(gridDim.x) * kInterWarps;
+  long long u = static_cast<long long>(blockIdx.x) * kInterWarps + warp;
   int64_t staged = -1;
   TreeInfo ti{1, 1, false};
   while (u < nunits) {
-    const long long u_next = next_ticket(p, lane);  // issued early, used next iteration
+    const long long u_next = next_ticket(p, lane) + nwarps_grid;  // issued early, used next iteration
     const int64_t tp = u / p.nch;
     const int c = static_cast<int>(u - tp * p.nch);
     if (tp != staged) {
@@ -947,7 +935,7 @@ __global__ void __launch_bounds__(32 * kIntraWarps, K >= 16 ? 2 : 4) k_intra(con
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    s_item[0] = static_cast<long long>(atomicAdd(&p.ctl->work, 1ull));
+    s_item[0] = static_cast<long long>(blockIdx.x);  // first item: static; then the queue (after the grid)
   }
   __syncthreads();
   const long long nitems = p.P * p.nseg;
@@ -962,7 +950,7 @@ __global__ void __launch_bounds__(32 * kIntraWarps, K >= 16 ? 2 : 4) k_intra(con
     // a4: TMA bulk copy of the compiled program row into shared memory,
     // completion signalled on an mbarrier; the row's metadata alongside
     if (threadIdx.x == 0) {
-      s_item[(it + 1) & 1] = static_cast<long long>(atomicAdd(&p.ctl->work, 1ull));
+      s_item[(it + 1) & 1] = static_cast<long long>(atomicAdd(&p.ctl->work, 1ull)) + gridDim.x;
       const uint32_t bar = smem_u32(&mbar);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(row_bytes) : "memory");

@@ -299,6 +299,10 @@ int launch(Plan& pl, int mode, const float* X, int32_t x_layout, const float* y,
   cudaError_t err = cudaLaunchKernel(fn, dim3(pl.grid), dim3(32 * pl.warps_per_cta), args, pl.smem_bytes, s);
   if (ev_end) cudaEventRecord(static_cast<cudaEvent_t>(ev_end), s);
   ++launches;
+  if (mode_reduce(mode) && kp.nparts > 1) {  // trees split over several units: fixed-order combine
+    launch_combine(kp, s);
+    ++launches;
+  }
   if (n_launches) *n_launches = launches;
   if (err == cudaSuccess) err = cudaGetLastError();
   if (err != cudaSuccess) {
