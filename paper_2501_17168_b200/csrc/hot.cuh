@@ -114,6 +114,24 @@ __device__ __forceinline__ float absmax(const u64 (&v)[N2]) {
   return m;
 }
 
+// max |x| over the finite-or-NaN points (+-inf skipped): the full-set copy
+// keeps infinite operands on the fast paths, whose values there equal the
+// library's (NaN for trig, IEEE for / and 1/x, inf for sqrt)
+template <int N2>
+__device__ __forceinline__ float absmax_noinf(const u64 (&v)[N2]) {
+  float m = 0.0f;
+#pragma unroll
+  for (int j = 0; j < N2; ++j) {
+    const float a = fabsf(lo(v[j])), b = fabsf(hi(v[j]));
+    m = fmaxf(m, fmaxf(a == kInf ? 0.0f : a, b == kInf ? 0.0f : b));
+  }
+  return m;
+}
+// a / b with an infinite operand: nu * MUFU.RCP(de) is the IEEE quotient
+__device__ __forceinline__ float div_inf_fix(float q, float nu, float de) {
+  return (fabsf(nu) == kInf || fabsf(de) == kInf) ? (fabsf(de) > kDelta ? __fmul_rn(nu, rcp_ftz(de)) : 1.0f) : q;
+}
+
 // ---- packed forms of fastmath.cuh (same operations, same order) ----
 // protected correctly rounded a / b on the fast range (div_fast per point);
 // nb = -b (exact)
@@ -229,14 +247,25 @@ __device__ __forceinline__ bool interp_hot(const Node* __restrict__ tree, int le
                            fmaxf(fabsf(lo(b[j])), fabsf(hi(b[j])))));                   \
       mn = fminf(mn, fminf(fabsf(lo(NUM[j])), fabsf(hi(NUM[j]))));                      \
     }                                                                                   \
-    bail |= !(mx <= kDivRange);                                                         \
+    bool with_inf = false;                                                              \
+    if (!(mx <= kDivRange)) { /* rare: re-check without the +-inf points */            \
+      bail |= !(fmaxf(absmax_noinf<N2>(t), absmax_noinf<N2>(b)) <= kDivRange);          \
+      with_inf = true;                                                                  \
+    }                                                                                   \
     if (mn < kDivRangeMin) {                                                            \
       FOR2 {                                                                            \
         bail |= (lo(NUM[j]) != 0.0f && fabsf(lo(NUM[j])) < kDivRangeMin) |              \
                 (hi(NUM[j]) != 0.0f && fabsf(hi(NUM[j])) < kDivRangeMin);               \
       }                                                                                 \
     }                                                                                   \
-    FOR2 t[j] = protect_div(div2(NUM[j], DEN[j], NDEN[j]), DEN[j]);                     \
+    if (with_inf) {                                                                     \
+      FOR2 {                                                                            \
+        const u64 q = protect_div(div2(NUM[j], DEN[j], NDEN[j]), DEN[j]);               \
+        t[j] = pk(div_inf_fix(lo(q), lo(NUM[j]), lo(DEN[j])), div_inf_fix(hi(q), hi(NUM[j]), hi(DEN[j]))); \
+      }                                                                                 \
+    } else {                                                                            \
+      FOR2 t[j] = protect_div(div2(NUM[j], DEN[j], NDEN[j]), DEN[j]);                   \
+    }                                                                                   \
   }
 #define DIV_CASES(HC, NUM, DEN)                                                         \
   case HC: {                                                                            \
@@ -269,7 +298,7 @@ __device__ __forceinline__ bool interp_hot(const Node* __restrict__ tree, int le
     if (__all_sync(FULL_MASK, m <= kSinCosSmall)) {                                     \
       FOR2 t[j] = pk(APPROX(lo(t[j])), APPROX(hi(t[j])));                               \
     } else {                                                                            \
-      bail |= !(m <= kTrigReduceMax);                                                   \
+      bail |= !(m <= kTrigReduceMax) && !(absmax_noinf<N2>(t) <= kTrigReduceMax);       \
       FOR2 {                                                                            \
         const u64 r = red2pi2(t[j]);                                                    \
         t[j] = pk(APPROX(lo(r)), APPROX(hi(r)));                                        \
@@ -282,7 +311,7 @@ __device__ __forceinline__ bool interp_hot(const Node* __restrict__ tree, int le
     if (__all_sync(FULL_MASK, m <= kTanSmall)) {                                        \
       FOR2 t[j] = poly_tan2(t[j]);                                                      \
     } else {                                                                            \
-      bail |= !(m <= kTrigReduceMax);                                                   \
+      bail |= !(m <= kTrigReduceMax) && !(absmax_noinf<N2>(t) <= kTrigReduceMax);       \
       FOR2 t[j] = tan_full2(t[j]);                                                      \
     }                                                                                   \
   }
@@ -352,12 +381,12 @@ __device__ __forceinline__ bool interp_hot(const Node* __restrict__ tree, int le
                 mn = min(mn, min((__float_as_uint(lo(t[j])) & 0x7FFFFFFFu) - 1u,
                                  (__float_as_uint(hi(t[j])) & 0x7FFFFFFFu) - 1u));
               }
-              bail |= !(mx <= kSqrtRange);
+              bail |= !(mx <= kSqrtRange) && !(absmax_noinf<N2>(t) <= kSqrtRange);  // sqrt(inf) = inf below
               bail |= mn < __float_as_uint(kSqrtRangeMin) - 1u;
               FOR2 t[j] = pk(hot_sqrt(lo(t[j])), hot_sqrt(hi(t[j])));
             })
             UN_CASES(HC_INV, {
-              bail |= !(absmax<N2>(t) <= kSqrtRange);
+              bail |= !(absmax_noinf<N2>(t) <= kSqrtRange);  // 1 / +-inf = +-0 below
               FOR2 t[j] = pk(hot_inv(lo(t[j])), hot_inv(hi(t[j])));
             })
             case HC_IF: {  // a = top, b = first pop, c = second pop

@@ -200,9 +200,11 @@ __device__ __forceinline__ float hot_ge(float a, float b) { return a >= b ? 1.0f
 // fast forms on their checked range (callers bail outside it)
 __device__ __forceinline__ float hot_sqrt(float x) {
   const float a = fabsf(x);
-  return a == 0.0f ? 0.0f : sqrt_fast(a);
+  return (a == 0.0f || a == kInf) ? a : sqrt_fast(a);  // = slow_sqrt at 0 and inf
 }
-__device__ __forceinline__ float hot_inv(float a) { return fabsf(a) > kDelta ? rcp_fast(a) : 0.0f; }
+__device__ __forceinline__ float hot_inv(float a) {
+  return fabsf(a) > kDelta ? (fabsf(a) == kInf ? copysignf(0.0f, a) : rcp_fast(a)) : 0.0f;
+}
 
 // The value a unary function gives a CONST operand c, exactly as the
 // interpreter computes it (fast path on its range, the library function
