@@ -86,50 +86,27 @@ struct alignas(8) Node {
 constexpr int kInterWarps = 4;
 constexpr int kIntraWarps = 8;
 
+// Hot code base of function id f (0..24: the 22 ids, then SUB_R, DIV_R,
+// POW_R), one byte each in four 64-bit words (branch-free: the compile pass
+// evaluates it per lane on divergent ops)
+EVOGP_HD inline uint32_t hot_base(uint32_t f) {
+  const uint64_t w = f < 8 ? 0x1b1917150c090603ull
+                           : (f < 16 ? 0x3d3b39373533211eull : (f < 24 ? 0x120f41302d2a273full : 0x24ull));
+  return static_cast<uint32_t>(w >> ((f & 7u) * 8u)) & 0xFFu;
+}
+
 // Hot code of a decoded single-output node word (op in bits 0-7, fuse flags
-// kFuse / kFuseVar). A unary node with a fused CONST leaf has no code here:
-// the compile pass folds it (returns HC_END as a marker).
+// kFuse / kFuseVar): leaves PUSH_C / PUSH_V; binary base + {S, C, V};
+// unary base + {T, V} (a fused CONST operand is folded by the compile pass:
+// HC_END is returned as a marker); IF: HC_IF.
 EVOGP_HD inline uint32_t hot_code_of(uint32_t w0) {
   const uint32_t op = w0 & 0xFFu;
-  if (op == OP_CONST) return HC_PUSH_C;
-  if (op == OP_VAR) return HC_PUSH_V;
-  const int f = static_cast<int>(op) - OP_FN;
+  const uint32_t f = op - OP_FN;  // wraps for leaves
   const uint32_t src = (w0 & kFuse) ? ((w0 & kFuseVar) ? 2u : 1u) : 0u;
-  uint32_t base;
-  switch (f) {
-    case F_ADD: base = HC_ADD; break;
-    case F_SUB: base = HC_SUB; break;
-    case F_MUL: base = HC_MUL; break;
-    case F_DIV: base = HC_DIV; break;
-    case F_SUB_R: base = HC_SUBR; break;
-    case F_DIV_R: base = HC_DIVR; break;
-    case F_MAX: base = HC_MAX; break;
-    case F_MIN: base = HC_MIN; break;
-    case F_POW: base = HC_POW; break;
-    case F_POW_R: base = HC_POWR; break;
-    case F_LT: base = HC_LT; break;
-    case F_GT: base = HC_GT; break;
-    case F_LE: base = HC_LE; break;
-    case F_GE: base = HC_GE; break;
-    case F_IF: return HC_IF;
-    default: {  // unary: T or V (a fused CONST operand is folded away)
-      uint32_t u;
-      switch (f) {
-        case F_SIN: u = HC_SIN; break;
-        case F_COS: u = HC_COS; break;
-        case F_TAN: u = HC_TAN; break;
-        case F_LOG: u = HC_LOG; break;
-        case F_EXP: u = HC_EXP; break;
-        case F_TANH: u = HC_TANH; break;
-        case F_NEG: u = HC_NEG; break;
-        case F_ABS: u = HC_ABS; break;
-        case F_SQRT: u = HC_SQRT; break;
-        default: u = HC_INV; break;
-      }
-      return src == 1u ? HC_END : u + (src == 2u ? 1u : 0u);
-    }
-  }
-  return base + src;
+  const bool unary = f < 22u && ((0x1FC70u >> f) & 1u);
+  const uint32_t fn = hot_base(f < 25u ? f : 0u) + (unary ? (src == 2u ? 1u : 0u) : (f == F_IF ? 0u : src));
+  const uint32_t code = (unary && src == 1u) ? static_cast<uint32_t>(HC_END) : fn;
+  return op == OP_CONST ? static_cast<uint32_t>(HC_PUSH_C) : (op == OP_VAR ? static_cast<uint32_t>(HC_PUSH_V) : code);
 }
 
 enum Mode : int { MODE_EVAL1 = 0, MODE_EVALN = 1, MODE_SSE = 2, MODE_CLS = 3 };
