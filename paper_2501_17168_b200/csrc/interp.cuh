@@ -752,12 +752,54 @@ __device__ __forceinline__ void store_out1(const KParams& p, int64_t tp, int64_t
   }
 }
 
+// Fast Modi store (K = 4, N outputs, a full 16-byte-aligned chunk): lane l
+// owns points 4l..4l+3, whose N outputs each are 4N contiguous floats of the
+// row; it reads its four points of every slot with one LDS.128 per slot and
+// writes them point-major with N STG.128 (a warp stores 512 N contiguous
+// bytes). Conflict-free, no index arithmetic per element.
+template <int N>
+__device__ __forceinline__ void store_outn_fast(float* o, const float* acc, int lane, bool valid) {
+  float v[N][4];
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    const float4 a = *reinterpret_cast<const float4*>(acc + r * 128 + 4 * lane);
+    v[r][0] = a.x;
+    v[r][1] = a.y;
+    v[r][2] = a.z;
+    v[r][3] = a.w;
+  }
+  float4* dst = reinterpret_cast<float4*>(o + 4 * lane * N);
+  const float nan = __int_as_float(0x7FC00000);
+#pragma unroll
+  for (int c = 0; c < N; ++c) {  // flat element e = 4c + i of the lane's run: point e / N, slot e % N
+    float e4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) e4[i] = valid ? v[(4 * c + i) % N][(4 * c + i) / N] : nan;
+    dst[c] = make_float4(e4[0], e4[1], e4[2], e4[3]);
+  }
+}
+
 // out[tp][d][o] from the per-warp accumulator acc[o][32K], written as one
 // contiguous, coalesced range of the row.
 template <int K>
 __device__ __forceinline__ void store_outn(const KParams& p, int64_t tp, int64_t chunk_base, int lane,
                                           const float* acc, bool valid) {
   __syncwarp();
+  if constexpr (K == 4) {
+    const int64_t base_el = (tp * p.D + chunk_base) * p.n_out;
+    float* o = p.out + base_el;
+    if (chunk_base + 128 <= p.D && p.n_out <= 6 && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
+      switch (p.n_out) {
+        case 2: store_outn_fast<2>(o, acc, lane, valid); break;
+        case 3: store_outn_fast<3>(o, acc, lane, valid); break;
+        case 4: store_outn_fast<4>(o, acc, lane, valid); break;
+        case 5: store_outn_fast<5>(o, acc, lane, valid); break;
+        default: store_outn_fast<6>(o, acc, lane, valid); break;
+      }
+      __syncwarp();
+      return;
+    }
+  }
   const int64_t npts = min(static_cast<int64_t>(32 * K), p.D - chunk_base);
   const unsigned cnt = static_cast<unsigned>(npts * p.n_out);
   float* o = p.out + (tp * p.D + chunk_base) * p.n_out;
