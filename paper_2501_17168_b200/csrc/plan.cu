@@ -100,36 +100,39 @@ int occupancy(const void* fn, int threads, size_t smem, int dev) {
 }  // namespace
 
 // Selector (c). PAPER P:356 compares D with the CUDA-core count (SMs x 128,
-// reading R11). On B200 that rule is replaced by the measured crossover
-// table (tools/calibrate_selector.py, selector_table.json, E1 methodology of
-// P:489-525): the entry nearest in (log L, log P) gives the smallest D from
-// which kernel (b) is consistently faster (0: never). Other GPUs fall back to
-// the paper's rule.
+// reading R11). On B200 that rule is replaced by measurement
+// (tools/calibrate_selector.py, selector_table.json, the E1 methodology of
+// P:489-525): the faster kernel of every measured (L, P, n_out, D) cell; a
+// call takes the nearest cell of its output class in (log L, log P, log D).
+// Other GPUs fall back to the paper's rule.
 struct SelectorEntry {
   int L;
   int64_t P;
-  int64_t crossover_D;
+  int n_out;
+  int64_t D;
+  int strategy;
 };
 #include "selector_table.inc"
 
 int select_strategy(int64_t P, int64_t D, int32_t L, int32_t n_out, int device) {
-  (void)n_out;  // calibrated with n_out = 1; used for Modi evaluation as well
   const int sms = num_sms(device);
   if (sms != 148) return D >= static_cast<int64_t>(sms) * 128 ? EVOGP_STRATEGY_INTRA : EVOGP_STRATEGY_INTER;
-  const double lL = std::log(std::max(L, 1)), lP = std::log(static_cast<double>(std::max<int64_t>(P, 1)));
-  const SelectorEntry* best = &kSelectorTable[0];
-  double bL = 1e300, bP = 1e300;
+  const double lL = std::log(std::max(L, 1)), lP = std::log(static_cast<double>(std::max<int64_t>(P, 1))),
+               lD = std::log(static_cast<double>(std::max<int64_t>(D, 1)));
+  const bool multi = n_out > 1;
+  int best = EVOGP_STRATEGY_INTER;
+  double bd = 1e300;
   for (const SelectorEntry& e : kSelectorTable) {
-    const double dL = std::fabs(std::log(static_cast<double>(e.L)) - lL);
-    const double dP = std::fabs(std::log(static_cast<double>(e.P)) - lP);
-    if (dL < bL - 1e-9 || (std::fabs(dL - bL) <= 1e-9 && dP < bP)) {
-      best = &e;
-      bL = dL;
-      bP = dP;
+    if ((e.n_out > 1) != multi) continue;
+    const double dL = std::log(static_cast<double>(e.L)) - lL, dP = std::log(static_cast<double>(e.P)) - lP,
+                 dD = std::log(static_cast<double>(e.D)) - lD;
+    const double d = dL * dL + dP * dP + dD * dD;
+    if (d < bd) {
+      bd = d;
+      best = e.strategy;
     }
   }
-  if (best->crossover_D <= 0) return EVOGP_STRATEGY_INTER;
-  return D >= best->crossover_D ? EVOGP_STRATEGY_INTRA : EVOGP_STRATEGY_INTER;
+  return best;
 }
 
 int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_t n_out, int mode, int strategy,
