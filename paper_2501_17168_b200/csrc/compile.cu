@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
         __syncwarp();
       }
     } else {
-      ti = stage_tree_warp(p, tp, row, lane, p.n_out == 1);  // single-output rows get hot codes
+      ti = stage_tree_warp(p, tp, row, lane, true);  // hot codes (multi-output rows: + Modi twins)
     }
   compiled:
     if (lane == 0) {

@@ -73,7 +73,8 @@ enum HotCode : uint32_t {
   HC_MAX = 27, HC_MIN = 30, HC_POW = 33, HC_POWR = 36, HC_LT = 39, HC_GT = 42, HC_LE = 45, HC_GE = 48,
   HC_LOG = 51, HC_EXP = 53, HC_TANH = 55, HC_NEG = 57, HC_ABS = 59, HC_SQRT = 61, HC_INV = 63,
   HC_IF = 65,
-  HC_COUNT = 66
+  HC_COUNT = 66,
+  HC_MODI = 66  // multi-output rows: a Modi node's code = its function's code + HC_MODI
 };
 constexpr uint32_t kHotShift = 24;
 
@@ -105,7 +106,8 @@ EVOGP_HD inline uint32_t hot_code_of(uint32_t w0) {
   const uint32_t src = (w0 & kFuse) ? ((w0 & kFuseVar) ? 2u : 1u) : 0u;
   const bool unary = f < 22u && ((0x1FC70u >> f) & 1u);
   const uint32_t fn = hot_base(f < 25u ? f : 0u) + (unary ? (src == 2u ? 1u : 0u) : (f == F_IF ? 0u : src));
-  const uint32_t code = (unary && src == 1u) ? static_cast<uint32_t>(HC_END) : fn;
+  const bool modi = ((w0 >> 8) & 0xFFu) != kNoSlot;  // multi-output rows only (never fused)
+  const uint32_t code = (unary && src == 1u) ? static_cast<uint32_t>(HC_END) : fn + (modi ? HC_MODI : 0u);
   return op == OP_CONST ? static_cast<uint32_t>(HC_PUSH_C) : (op == OP_VAR ? static_cast<uint32_t>(HC_PUSH_V) : code);
 }
 

@@ -176,6 +176,91 @@ __device__ __forceinline__ u64 tan_full2(u64 x) {  // fm_tan_fast per point
 
 #include "hot_ptx.inc"
 
+// Multi-output rows (Modi, reading R4) at K = 4: the inline-PTX
+// loop (hot_ptx.inc) runs every node except the four functions with CUDA
+// libm bodies; at one of those it returns the node (esc = its hot code,
+// ew0 = its word, pn / top advanced) and this loop applies the library
+// function — the same code as every other copy — with the Modi epilogue,
+// then re-enters. accl: the lane's Modi accumulators (slot stride 32 K).
+template <int K>
+__device__ __forceinline__ bool interp_multi(const Node* __restrict__ tree, int len, const float* __restrict__ xl,
+                                             float* stk, float* accl, float (&out)[K]) {
+  static_assert(K == 4, "multi-output packed loop: K = 4");
+  constexpr int N2 = K / 2;
+  constexpr int SLOT = 32 * K;
+  u64 t[N2];
+  {
+    const Node nd = tree[len];  // node len-1: a leaf
+    if ((nd.w0 & 0xFFu) == OP_CONST) {
+      const u64 c = splat(__uint_as_float(nd.w1));
+#pragma unroll
+      for (int j = 0; j < N2; ++j) t[j] = c;
+    } else {
+      ldx<K>(xl + nd.w1, t);
+    }
+  }
+  uint32_t pn = static_cast<uint32_t>(__cvta_generic_to_shared(tree + len - 1));
+  uint32_t top = static_cast<uint32_t>(__cvta_generic_to_shared(stk));
+  const uint32_t top0 = top;
+  const uint32_t accb = static_cast<uint32_t>(__cvta_generic_to_shared(accl));
+  uint32_t bail = 0;
+  for (;;) {
+    uint32_t esc, ew0;
+    bail |= interp_multi_ptx_k4(pn, top, xl, accb, t, esc, ew0);
+    if (esc == 0) break;
+    const bool modi = esc >= HC_MODI;
+    const uint32_t c = modi ? esc - HC_MODI : esc;
+    float a[K], rt[K];
+#pragma unroll
+    for (int j = 0; j < N2; ++j) unpk(t[j], a[2 * j], a[2 * j + 1]);
+    if (c == HC_POW) {  // pow(|a|, b), b popped (the rightmost child)
+      top -= SLOT * 4;
+      vld<K>(stk + (top - top0) / 4, rt);
+      float e[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) e[k] = rt[k];
+#pragma unroll 1
+      for (int it = 0; it < K; ++it) {  // one inlined powf body, register rotation
+        const float v = powf(fabsf(a[0]), e[0]);
+        const float e0 = e[0];
+#pragma unroll
+        for (int k = 0; k < K - 1; ++k) {
+          a[k] = a[k + 1];
+          e[k] = e[k + 1];
+        }
+        a[K - 1] = v;
+        e[K - 1] = e0;
+      }
+    } else {  // unary: the operand is the rightmost child
+#pragma unroll
+      for (int k = 0; k < K; ++k) rt[k] = a[k];
+#pragma unroll 1
+      for (int it = 0; it < K; ++it) {
+        const float v = c == HC_LOG ? fn_plog(a[0]) : (c == HC_EXP ? expf(a[0]) : tanhf(a[0]));
+#pragma unroll
+        for (int k = 0; k < K - 1; ++k) a[k] = a[k + 1];
+        a[K - 1] = v;
+      }
+    }
+    if (modi) {  // out[slot] += value; the rightmost child's value goes up
+      float* acc = accl + ((ew0 >> 8) & 0xFFu) * SLOT;
+      float av[K];
+      vld<K>(acc, av);
+#pragma unroll
+      for (int k = 0; k < K; ++k) av[k] = __fadd_rn(av[k], a[k]);
+      vst<K>(acc, av);
+#pragma unroll
+      for (int j = 0; j < N2; ++j) t[j] = pk(rt[2 * j], rt[2 * j + 1]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < N2; ++j) t[j] = pk(a[2 * j], a[2 * j + 1]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < N2; ++j) unpk(t[j], out[2 * j], out[2 * j + 1]);
+  return bail != 0;
+}
+
 template <int K, bool PAPER>
 __device__ __forceinline__ bool interp_hot(const Node* __restrict__ tree, int len, const float* __restrict__ xl,
                                            float* stk, float (&out)[K]) {

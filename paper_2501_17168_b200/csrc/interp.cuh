@@ -688,6 +688,8 @@ __device__ __forceinline__ void run_chunk(const KParams& p, const Node* tree, co
       // single-output programs carry hot codes (compile pass): packed interpreter
       bail = ti.paper ? hot::interp_hot<K, true>(tree, ti.len, xl, s_stack_l, tos)
                       : hot::interp_hot<K, false>(tree, ti.len, xl, s_stack_l, tos);
+    } else if constexpr (MULTI && K == 4) {
+      bail = hot::interp_multi<K>(tree, ti.len, xl, s_stack_l, s_acc_l, tos);
     } else {
       bail = ti.paper ? interpret<K, MULTI, false, true>(tree, ti.len, xl, s_stack_l, s_acc_l, tos)
                       : interpret<K, MULTI, false>(tree, ti.len, xl, s_stack_l, s_acc_l, tos);
