@@ -176,7 +176,7 @@ __device__ __forceinline__ u64 tan_full2(u64 x) {  // fm_tan_fast per point
 
 #include "hot_ptx.inc"
 
-// Multi-output rows (Modi, reading R4) at K = 4: the inline-PTX
+// Multi-output rows (Modi, reading R4) at K = 4 or 8: the inline-PTX
 // loop (hot_ptx.inc) runs every node except the four functions with CUDA
 // libm bodies; at one of those it returns the node (esc = its hot code,
 // ew0 = its word, pn / top advanced) and this loop applies the library
@@ -185,7 +185,7 @@ __device__ __forceinline__ u64 tan_full2(u64 x) {  // fm_tan_fast per point
 template <int K>
 __device__ __forceinline__ bool interp_multi(const Node* __restrict__ tree, int len, const float* __restrict__ xl,
                                              float* stk, float* accl, float (&out)[K]) {
-  static_assert(K == 4, "multi-output packed loop: K = 4");
+  static_assert(K == 4 || K == 8, "multi-output packed loop: K = 4 or 8");
   constexpr int N2 = K / 2;
   constexpr int SLOT = 32 * K;
   u64 t[N2];
@@ -206,7 +206,11 @@ __device__ __forceinline__ bool interp_multi(const Node* __restrict__ tree, int 
   uint32_t bail = 0;
   for (;;) {
     uint32_t esc, ew0;
-    bail |= interp_multi_ptx_k4(pn, top, xl, accb, t, esc, ew0);
+    if constexpr (K == 4) {
+      bail |= interp_multi_ptx_k4(pn, top, xl, accb, t, esc, ew0);
+    } else {
+      bail |= interp_multi_ptx_k8(pn, top, xl, accb, t, esc, ew0);
+    }
     if (esc == 0) break;
     const bool modi = esc >= HC_MODI;
     const uint32_t c = modi ? esc - HC_MODI : esc;
@@ -234,13 +238,22 @@ __device__ __forceinline__ bool interp_multi(const Node* __restrict__ tree, int 
     } else {  // unary: the operand is the rightmost child
 #pragma unroll
       for (int k = 0; k < K; ++k) rt[k] = a[k];
-#pragma unroll 1
-      for (int it = 0; it < K; ++it) {
-        const float v = c == HC_LOG ? fn_plog(a[0]) : (c == HC_EXP ? expf(a[0]) : tanhf(a[0]));
-#pragma unroll
-        for (int k = 0; k < K - 1; ++k) a[k] = a[k + 1];
-        a[K - 1] = v;
+      // one branch per function (warp-uniform), each one inlined body applied
+      // to the K points by register rotation (a select would evaluate all three)
+#define EVOGP_ROT(FN)                                             \
+  _Pragma("unroll 1") for (int it = 0; it < K; ++it) {            \
+    const float v = FN(a[0]);                                     \
+    _Pragma("unroll") for (int k = 0; k < K - 1; ++k) a[k] = a[k + 1]; \
+    a[K - 1] = v;                                                 \
+  }
+      if (c == HC_LOG) {
+        EVOGP_ROT(fn_plog)
+      } else if (c == HC_EXP) {
+        EVOGP_ROT(expf)
+      } else {
+        EVOGP_ROT(tanhf)
       }
+#undef EVOGP_ROT
     }
     if (modi) {  // out[slot] += value; the rightmost child's value goes up
       float* acc = accl + ((ew0 >> 8) & 0xFFu) * SLOT;

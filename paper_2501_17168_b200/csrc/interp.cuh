@@ -688,7 +688,7 @@ __device__ __forceinline__ void run_chunk(const KParams& p, const Node* tree, co
       // single-output programs carry hot codes (compile pass): packed interpreter
       bail = ti.paper ? hot::interp_hot<K, true>(tree, ti.len, xl, s_stack_l, tos)
                       : hot::interp_hot<K, false>(tree, ti.len, xl, s_stack_l, tos);
-    } else if constexpr (MULTI && K == 4) {
+    } else if constexpr (MULTI && (K == 4 || K == 8)) {
       bail = hot::interp_multi<K>(tree, ti.len, xl, s_stack_l, s_acc_l, tos);
     } else {
       bail = ti.paper ? interpret<K, MULTI, false, true>(tree, ti.len, xl, s_stack_l, s_acc_l, tos)
@@ -760,11 +760,11 @@ __device__ __forceinline__ void store_out1(const KParams& p, int64_t tp, int64_t
 // writes them point-major with N STG.128 (a warp stores 512 N contiguous
 // bytes). Conflict-free, no index arithmetic per element.
 template <int N>
-__device__ __forceinline__ void store_outn_fast(float* o, const float* acc, int lane, bool valid) {
+__device__ __forceinline__ void store_outn_fast(float* o, const float* acc, int slot_stride, int lane, bool valid) {
   float v[N][4];
 #pragma unroll
   for (int r = 0; r < N; ++r) {
-    const float4 a = *reinterpret_cast<const float4*>(acc + r * 128 + 4 * lane);
+    const float4 a = *reinterpret_cast<const float4*>(acc + r * slot_stride + 4 * lane);
     v[r][0] = a.x;
     v[r][1] = a.y;
     v[r][2] = a.z;
@@ -787,16 +787,21 @@ template <int K>
 __device__ __forceinline__ void store_outn(const KParams& p, int64_t tp, int64_t chunk_base, int lane,
                                           const float* acc, bool valid) {
   __syncwarp();
-  if constexpr (K == 4) {
+  if constexpr (K == 4 || K == 8) {  // groups of 128 points: lane l owns points 128 g + 4 l + j
     const int64_t base_el = (tp * p.D + chunk_base) * p.n_out;
     float* o = p.out + base_el;
-    if (chunk_base + 128 <= p.D && p.n_out <= 6 && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
-      switch (p.n_out) {
-        case 2: store_outn_fast<2>(o, acc, lane, valid); break;
-        case 3: store_outn_fast<3>(o, acc, lane, valid); break;
-        case 4: store_outn_fast<4>(o, acc, lane, valid); break;
-        case 5: store_outn_fast<5>(o, acc, lane, valid); break;
-        default: store_outn_fast<6>(o, acc, lane, valid); break;
+    if (chunk_base + 32 * K <= p.D && p.n_out <= 6 && (reinterpret_cast<uintptr_t>(o) & 15u) == 0) {
+#pragma unroll
+      for (int g = 0; g < K / 4; ++g) {
+        float* og = o + g * 128 * p.n_out;
+        const float* ag = acc + g * 128;
+        switch (p.n_out) {
+          case 2: store_outn_fast<2>(og, ag, 32 * K, lane, valid); break;
+          case 3: store_outn_fast<3>(og, ag, 32 * K, lane, valid); break;
+          case 4: store_outn_fast<4>(og, ag, 32 * K, lane, valid); break;
+          case 5: store_outn_fast<5>(og, ag, 32 * K, lane, valid); break;
+          default: store_outn_fast<6>(og, ag, 32 * K, lane, valid); break;
+        }
       }
       __syncwarp();
       return;
@@ -911,7 +916,8 @@ __device__ __forceinline__ long long next_ticket(const KParams& p, int lane) {
 }
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(32 * kInterWarps, K >= 16 ? 5 : 8) k_inter(const KParams p) {
+__global__ void __launch_bounds__(32 * kInterWarps, (K >= 16 || (K == 8 && mode_multi(MODE))) ? 4 : 8)
+    k_inter(const KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int V = Lay<K>::V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -963,7 +969,8 @@ __device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
 }
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(32 * kIntraWarps, K >= 16 ? 2 : 4) k_intra(const KParams p) {
+__global__ void __launch_bounds__(32 * kIntraWarps, (K >= 16 || (K == 8 && mode_multi(MODE))) ? 2 : 4)
+    k_intra(const KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
   __shared__ double s_red[kIntraWarps];

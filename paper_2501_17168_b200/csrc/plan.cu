@@ -56,13 +56,13 @@ const void* kernel_ptr(int strategy, int K, int mode) {
       case 1: return kernel_inter_k1(mode);
       case 2: return kernel_inter_k2(mode);
       case 4: return kernel_inter_k4(mode);
-      case 8: return multi ? nullptr : kernel_inter_k8(mode);
+      case 8: return kernel_inter_k8(mode);
       case 16: return multi ? nullptr : kernel_inter_k16(mode);
     }
     return nullptr;
   }
   if (K == 16 && !multi) return kernel_intra_k16(mode);
-  if (K == 8 && !multi) return kernel_intra_k8(mode);
+  if (K == 8) return kernel_intra_k8(mode);
   if (K == 4) return kernel_intra_k4(mode);
   return nullptr;
 }
@@ -156,12 +156,13 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   // tuning knobs for the calibration sweeps: datapoints
   // per lane and the resident-warps target that sizes the shared-memory stack
   const evogp_tuning& tu = tuning();
-  if (!multi && (tu.K == 4 || tu.K == 8 || tu.K == 16) && (strategy == EVOGP_STRATEGY_INTRA || D > 128)) K = tu.K;
+  if ((tu.K == 4 || tu.K == 8 || (tu.K == 16 && !multi)) && (strategy == EVOGP_STRATEGY_INTRA || D > 128)) K = tu.K;
   // resident-warp target: 32 (the K=8 register limit) once the compile pass
   // reorders deep programs; measured in profiles/sweep_kw_r01.txt
   // (K = 16 kernels hold twice the registers: 20 resident warps for (a), 16 for (b))
   int target_warps = tu.target_warps > 0 ? std::max(4, std::min(64, tu.target_warps))
-                                         : (K >= 16 ? (strategy == EVOGP_STRATEGY_INTER ? 20 : 16) : 32);
+                                         : (K >= 16 ? (strategy == EVOGP_STRATEGY_INTER ? 20 : 16)
+                                                    : (K == 8 && multi ? 16 : 32));
   const int warps = strategy == EVOGP_STRATEGY_INTER ? kInterWarps : kIntraWarps;
   const int64_t chunk = 32 * K;
   const int64_t nch = (D + chunk - 1) / chunk;
