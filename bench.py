@@ -328,8 +328,9 @@ def run_loop(args, cfg):
     P = cfg.P
     # island model across ranks: rank r evolves its own P trees
     seed = cfg.seed + 1_000_003 * rank
-    strategy = evogp.select_strategy(P, cfg.D, cfg.max_len, 1, local)
     ws = evogp.Workspace(P, cfg.D, cfg.max_len, cfg.n_in, 1, device=dev)
+    # selector (c) keyed on the population's own tree lengths (gp.selector_strategy)
+    strategy = evogp.Evolution(P, gp, Xd, yd, seed=seed).strategy
 
     launches = [0]
 

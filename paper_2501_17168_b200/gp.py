@@ -154,6 +154,21 @@ def reproduce(pop, fitness, n_children: int, cfg: GPConfig, seed: int, child0: i
     return t, v, s, par, ops
 
 
+def selector_strategy(pop, D: int) -> str:
+    """Selector (c) for a population whose trees may be much shorter than its
+    row length: the calibration (tools/calibrate_selector.py) draws tree
+    lengths uniformly in [L/2, L] (mean 0.75 L), so the table is keyed on the
+    row length a population of this mean length would have. One device
+    reduction + sync (call it outside timed loops)."""
+    from . import select_strategy
+
+    t, v, s = pop
+    P, L = int(s.shape[0]), int(s.shape[1])
+    mean = float(s[:, 0].float().mean().item()) if P else float(L)
+    L_eff = max(1, min(L, int(round(mean / 0.75))))
+    return select_strategy(P, D, L_eff)
+
+
 class Evolution:
     """Algorithm 1 for symbolic regression, device-resident:
     generation -> [fitness (fused SR MSE) -> reproduce] x G. Two population
@@ -173,6 +188,8 @@ class Evolution:
         generate(P, cfg, seed, device=dev, out=self.bufs[0])
         self.fitness = torch.empty(P, dtype=torch.float64, device=dev)
         self.generation = 0
+        if strategy == "auto":
+            self.strategy = selector_strategy(self.bufs[0], int(X.shape[0]))
 
     @property
     def population(self):

@@ -34,7 +34,7 @@ sys.path.insert(0, ROOT)
 import paper_2501_17168_b200 as evogp  # noqa: E402
 import synth  # noqa: E402
 
-WORK_CAP = 4e10  # node x datapoint steps per timed call
+WORK_CAP = 1.2e11  # node x datapoint steps per timed call (C3 itself, 1e11, is a cell)
 OUT_CAP = 8 << 30  # eval output bytes (n_out > 1)
 NODE_CAP = 2e8  # nodes per population (host generation + tensorize)
 
