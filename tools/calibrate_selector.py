@@ -6,7 +6,7 @@ Times forced kernel (a) (inter) and forced kernel (b) (intra) over the grid
   L in {15, 63, 127, 512} x P in {1e2 .. 1e6} x n_out in {1, 6} x D = 2^5 .. 2^22
 (single output: evogp_sr_fitness on the M-paper mix; six outputs: Modi
 evogp_eval on the M-full mix, p_modi 0.1 — the C2-C4 / C5 workloads), capped
-at 4e10 node x datapoint steps and 8 GB of outputs per call. Each cell is the
+at 1.2e11 node x datapoint steps and 8 GB of outputs per call. Each cell is the
 median of 5 CUDA-event timings after 2 warm-ups.
 
 The library's rule is a lookup table of the faster kernel per measured cell,
