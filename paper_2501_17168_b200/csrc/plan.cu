@@ -180,8 +180,15 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   // SM's 228 KB with the 1 KB the runtime reserves per CTA (per-warp sizing
   // rounded c3 down to 3 CTAs = 24 warps; this gives 4 CTAs: +11% on c3)
   int SD;
+  // shared memory an SM gives its CTAs: 228 KB minus the runtime's 1 KB per
+  // CTA and the kernel's static shared memory (k_inter: 4 mbarriers)
+  auto warp_budget = [&](int tw) {
+    const int ctas = std::max(1, tw / kInterWarps);
+    return (228 * 1024 - ctas * (1024 + 64)) / tw;
+  };
   if (strategy == EVOGP_STRATEGY_INTER) {
-    SD = ((227 * 1024) / target_warps - acc_bytes - tree_bytes) / slot_bytes;
+    // two program buffers per warp (current + prefetched, k_inter)
+    SD = (warp_budget(target_warps) - acc_bytes - 2 * tree_bytes) / slot_bytes;
     // long rows: each warp's staged program eats the stack budget (4 KB at
     // L = 512 leaves SD = 3 at 32 warps, and most evolved rows then run the
     // 2-pass split). Trade resident warps for at least kMinSlots slots
@@ -189,9 +196,10 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
     // 3.24e12 GPops/s kernel); short rows keep the 32-warp target.
     constexpr int kMinSlots = 5;
     if (SD < kMinSlots && tu.target_warps <= 0) {
-      const int per_warp = acc_bytes + tree_bytes + kMinSlots * slot_bytes;
+      const int per_warp = acc_bytes + 2 * tree_bytes + kMinSlots * slot_bytes;
       target_warps = std::max(16, (227 * 1024) / per_warp);
-      SD = ((227 * 1024) / target_warps - acc_bytes - tree_bytes) / slot_bytes;
+      while (target_warps > 16 && warp_budget(target_warps) < per_warp) --target_warps;
+      SD = (warp_budget(target_warps) - acc_bytes - 2 * tree_bytes) / slot_bytes;
     }
   } else {
     const int ctas = std::max(1, target_warps / warps);
@@ -201,7 +209,7 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   SD = std::max(2, std::min(SD, std::max(1, depth - 1)));
   const int warp_smem = acc_bytes + SD * slot_bytes;
   const size_t smem = strategy == EVOGP_STRATEGY_INTER
-                          ? static_cast<size_t>(warps) * (tree_bytes + warp_smem)
+                          ? static_cast<size_t>(warps) * (2 * tree_bytes + warp_smem)
                           : static_cast<size_t>(tree_bytes) +
                                 static_cast<size_t>(warps) * warp_smem;
   if (smem > 227 * 1024) return EVOGP_E_UNSUPPORTED;

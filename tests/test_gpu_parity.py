@@ -919,3 +919,36 @@ def test_multi_output_deep_rows_multipass():
         assert same_bits_mod_zero(g, r32).all(), strategy
         acc = evogp.classification_accuracy(*dev, Xd, ld, n_out, strategy=strategy).cpu().numpy()
         assert np.array_equal(acc, acc_ref), strategy
+
+
+def test_multi_output_infinite_operands_hot():
+    """Multi-output rows keep +-inf operands on the packed loop's fast paths:
+    a Modi DIV with infinite numerators or denominators (and finite points
+    beside them) gives the IEEE quotient, bit-identical to the FP32-faithful
+    oracle, with no chunk re-run cold (the fix-up must read the operands, not
+    the fast quotient)."""
+    evogp = _evogp()
+    n_in, n_out, D = 2, 3, 4096
+    # [M(o0,+), DIV, x0, x1, x1]  and  [M(o1,/), x1, x0]
+    tys = [[3 | 8, 3, 1, 1, 1], [3 | 8 | (1 << 8), 1, 1]]
+    vas = [[0, 3, 0, 1, 1], [3, 1, 0]]
+    pt = synth.PrefixTrees(np.cumsum([0] + [len(t) for t in tys]).astype(np.int64),
+                           np.array([x for t in tys for x in t], np.int16),
+                           np.array([x for v in vas for x in v], np.float32))
+    rng = np.random.default_rng(5)
+    X = rng.uniform(-3.0, 3.0, (D, n_in)).astype(np.float32)
+    X[::9, 0] = np.inf
+    X[4::9, 0] = -np.inf
+    X[7::13, 1] = np.inf
+    dt = to_device(pt, 5, n_in, n_out)
+    t, v, s = oracle_arrays(pt, 5, n_in, n_out)
+    r32 = oracle.evaluate(t, v, s, X, n_out=n_out, mode=1)
+    for strategy in ("inter", "intra"):
+        ws = evogp.Workspace(2, D, 5, n_in, n_out, device="cuda")
+        tt, vv, ss = dt
+        g = evogp.eval(tt, vv, ss, torch.from_numpy(X).cuda(), n_outputs=n_out, strategy=strategy,
+                       workspace=ws).cpu().numpy()
+        off = ws.ptr - ws.buf.data_ptr()
+        assert int(ws.buf[off + 4: off + 8].view(torch.int32).item()) == 0, strategy  # nothing re-ran cold
+        ok = same_bits_mod_zero(g, r32)
+        assert ok.all(), (strategy, (~ok).sum(), np.argwhere(~ok)[:4])
