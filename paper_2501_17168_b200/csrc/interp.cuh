@@ -923,80 +923,32 @@ template <int K, int MODE>
 __global__ void __launch_bounds__(32 * kInterWarps, (K >= 16 || (K == 8 && mode_multi(MODE))) ? 4 : 8)
     k_inter(const KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ __align__(8) uint64_t s_mbar[kInterWarps];
   constexpr int V = Lay<K>::V;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // per warp: two program buffers (the current tree's and the next unit's,
-  // prefetched by a TMA bulk copy while this unit is evaluated) | stacks
-  unsigned char* wbase = smem + static_cast<size_t>(warp) * (2 * p.tree_bytes + p.warp_smem_bytes);
-  Node* s_buf[2] = {reinterpret_cast<Node*>(wbase), reinterpret_cast<Node*>(wbase + p.tree_bytes)};
-  float* s_stack_l = reinterpret_cast<float*>(wbase + 2 * p.tree_bytes) + lane * V;
+  unsigned char* wbase = smem + static_cast<size_t>(warp) * (p.tree_bytes + p.warp_smem_bytes);
+  Node* s_tree = reinterpret_cast<Node*>(wbase);
+  float* s_stack_l = reinterpret_cast<float*>(wbase + p.tree_bytes) + lane * V;
   float* s_acc_l = s_stack_l + p.SD * 32 * K;
-  const uint32_t bar = smem_u32(&s_mbar[warp]);
-  if (lane == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
   const long long nunits = p.P * p.nch;
-  const uint32_t row_bytes = static_cast<uint32_t>(p.prog_ld) * 8u;  // 16-byte multiple
   // first unit: the warp's global index (no atomic); then the shared queue,
-  // whose tickets start after the grid's warps. Tickets run one unit ahead of
-  // the prefetch, which runs one unit ahead of the evaluation.
+  // whose tickets start after the grid's warps
   const long long nwarps_grid = static_cast<long long>(gridDim.x) * kInterWarps;
   long long u = static_cast<long long>(blockIdx.x) * kInterWarps + warp;
-  long long u1 = next_ticket(p, lane) + nwarps_grid;
-  int b = 0;                   // buffer holding `staged`
-  int64_t staged = -1, pre = -1;  // tree in s_buf[b] / prefetched into s_buf[1 - b]
-  uint32_t phase = 0;
-  TreeMeta pre_meta{1, -1};
+  int64_t staged = -1;
   TreeInfo ti{1, 1, false};
   while (u < nunits) {
-    const long long u2 = next_ticket(p, lane) + nwarps_grid;  // used two iterations on
-    const int64_t tp = u / p.nch;
+    const long long u_next = next_ticket(p, lane) + nwarps_grid;  // issued early, used next iteration
+    // unit -> (tree, chunk): 32-bit division whenever the unit count fits
+    // (a 64-bit division is a ~70-instruction call), none for one chunk
+    const int64_t tp = p.nch == 1 ? u : (nunits <= 0xFFFFFFFFll ? static_cast<int64_t>(static_cast<uint32_t>(u) /
+                                                                                   static_cast<uint32_t>(p.nch))
+                                                                : u / p.nch);
     const int c = static_cast<int>(u - tp * p.nch);
     if (tp != staged) {
-      if (tp == pre) {  // the prefetched row: wait for its bulk copy
-        if (lane == 0) {
-          uint32_t done = 0;
-          while (!done) {
-            asm volatile(
-                "{\n .reg .pred P1;\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n selp.u32 %0, 1, 0, "
-                "P1;\n}\n"
-                : "=r"(done)
-                : "r"(bar), "r"(phase)
-                : "memory");
-          }
-        }
-        phase ^= 1u;
-        __syncwarp();
-        b ^= 1;
-        ti = TreeInfo{pre_meta.len, pre_meta.maxdepth & (kPaperRow - 1), pre_meta.maxdepth >= 0,
-                      pre_meta.maxdepth >= 0 && (pre_meta.maxdepth & kPaperRow)};
-        pre = -1;
-      } else {
-        __syncwarp();
-        ti = load_program_warp(p, tp, s_buf[b], lane);
-      }
+      __syncwarp();
+      ti = load_program_warp(p, tp, s_tree, lane);
       staged = tp;
     }
-    // prefetch the next unit's row into the other buffer (its previous
-    // contents were last read before the __syncwarp that ended that unit)
-    const int64_t tp1 = u1 < nunits ? u1 / p.nch : -1;
-    if (tp1 >= 0 && tp1 != staged && tp1 != pre) {
-      pre_meta = p.info[tp1];
-      if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(row_bytes) : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(s_buf[b ^ 1])),
-            "l"(p.prog + tp1 * p.prog_ld), "r"(row_bytes), "r"(bar)
-            : "memory");
-      }
-      pre = tp1;
-    }
-    Node* s_tree = s_buf[b];
     const int64_t chunk_base = static_cast<int64_t>(c) * (32 * K);
     float tos[K];
     if (mode_multi(MODE) && !ti.valid) zero_acc<K>(s_acc_l, p.n_out);
@@ -1012,21 +964,7 @@ __global__ void __launch_bounds__(32 * kInterWarps, (K >= 16 || (K == 8 && mode_
       s = warp_sum_d(s);
       combine_partial(p, tp, c, s, lane);
     }
-    __syncwarp();
-    u = u1;
-    u1 = u2;
-  }
-  // an issued prefetch that was never consumed must complete before exit
-  if (pre >= 0 && lane == 0) {
-    uint32_t done = 0;
-    while (!done) {
-      asm volatile(
-          "{\n .reg .pred P1;\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n selp.u32 %0, 1, 0, "
-          "P1;\n}\n"
-          : "=r"(done)
-          : "r"(bar), "r"(phase)
-          : "memory");
-    }
+    u = u_next;
   }
 }
 

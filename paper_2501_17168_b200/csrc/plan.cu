@@ -186,9 +186,11 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
     const int ctas = std::max(1, tw / kInterWarps);
     return (228 * 1024 - ctas * (1024 + 64)) / tw;
   };
+  // one program-row buffer per warp (a TMA prefetch of the next unit's row
+  // into a second buffer measured slower: c2 kernel 3.78 vs 4.07e12, c4 -3%)
+  constexpr int nbuf = 1;
   if (strategy == EVOGP_STRATEGY_INTER) {
-    // two program buffers per warp (current + prefetched, k_inter)
-    SD = (warp_budget(target_warps) - acc_bytes - 2 * tree_bytes) / slot_bytes;
+    SD = (warp_budget(target_warps) - acc_bytes - nbuf * tree_bytes) / slot_bytes;
     // long rows: each warp's staged program eats the stack budget (4 KB at
     // L = 512 leaves SD = 3 at 32 warps, and most evolved rows then run the
     // 2-pass split). Trade resident warps for at least kMinSlots slots
@@ -196,10 +198,10 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
     // 3.24e12 GPops/s kernel); short rows keep the 32-warp target.
     constexpr int kMinSlots = 5;
     if (SD < kMinSlots && tu.target_warps <= 0) {
-      const int per_warp = acc_bytes + 2 * tree_bytes + kMinSlots * slot_bytes;
+      const int per_warp = acc_bytes + nbuf * tree_bytes + kMinSlots * slot_bytes;
       target_warps = std::max(16, (227 * 1024) / per_warp);
       while (target_warps > 16 && warp_budget(target_warps) < per_warp) --target_warps;
-      SD = (warp_budget(target_warps) - acc_bytes - 2 * tree_bytes) / slot_bytes;
+      SD = (warp_budget(target_warps) - acc_bytes - nbuf * tree_bytes) / slot_bytes;
     }
   } else {
     const int ctas = std::max(1, target_warps / warps);
@@ -209,7 +211,7 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   SD = std::max(2, std::min(SD, std::max(1, depth - 1)));
   const int warp_smem = acc_bytes + SD * slot_bytes;
   const size_t smem = strategy == EVOGP_STRATEGY_INTER
-                          ? static_cast<size_t>(warps) * (2 * tree_bytes + warp_smem)
+                          ? static_cast<size_t>(warps) * (nbuf * tree_bytes + warp_smem)
                           : static_cast<size_t>(tree_bytes) +
                                 static_cast<size_t>(warps) * warp_smem;
   if (smem > 227 * 1024) return EVOGP_E_UNSUPPORTED;
