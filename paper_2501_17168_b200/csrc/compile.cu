@@ -109,54 +109,66 @@ __device__ int reorder_program(const Node* s_nodes, int n, Node* row, unsigned c
   return depth;
 }
 
-// Warp-parallel Sethi-Ullman reordering + leaf fusion of a single-output
-// row, written straight into its program row (same decisions as
-// reorder_program followed by fuse_copy). Used when the caller's subtree
-// sizes are consistent — always the case for rows made by evogp_tensorize /
-// evogp_reproduce; checked here in parallel: a leaf has size 1 and walking a
-// node's children by their sizes ends exactly at i + size[i] (by induction
-// from the last node this makes every size the true one). Lanes own 32
-// consecutive nodes:
-//  * needs bottom-up, chunks from the last to the first: in-chunk children
-//    are read by shuffles, iterating until every node is known (children in
-//    later chunks are final, in shared memory);
-//  * new positions top-down: np[j] = j + acc[j], acc[j] = acc[parent] +
-//    (parent swapped ? (j first child ? +size(second) : -size(first)) : 0):
-//    pointer jumping over in-chunk parents by shuffles (5 rounds), chunks
-//    from the first;
+// Warp-parallel reordering + leaf fusion of a single-output row, written
+// straight into its program row (same decisions as reorder_program followed
+// by fuse_copy, with the larger-subtree-first order). Used when the caller's
+// subtree sizes are consistent — always the case for rows made by
+// evogp_tensorize / evogp_reproduce; checked here in parallel: a leaf has
+// size 1 and walking a node's children by their sizes ends exactly at
+// i + size[i] (by induction from the last node this makes every size the
+// true one). Lanes own 32 consecutive nodes:
+//  * order: a binary node whose first child's subtree is larger swaps its
+//    children (evaluates the larger one first);
+//  * new positions np[j] = j + acc[j]: a swapped node a moves its first
+//    child's subtree [c1, c2) by +size(c2) and its second's [c2, a+size(a))
+//    by -size(c1), so acc is the prefix sum of a difference array with three
+//    entries per swapped node (shared atomics), one warp scan per 32 nodes;
 //  * fusion: a unary / binary node absorbs its first-visited child when that
-//    is a leaf that is not the last node; positions are compacted by a
-//    prefix count of the absorbed leaves over new positions;
+//    is a leaf that is not the last node, else a binary node its second-
+//    visited leaf; positions are compacted by a prefix count of the absorbed
+//    leaves over new positions;
 //  * scatter of the final words to the global row.
+// Arities come from the decoded words (w0 bits 20-21).
 // Returns the new length (and *depth_out), or -1 when the sizes are
-// inconsistent. Scratch after the decoded nodes: 10 L bytes.
+// inconsistent. Scratch after the decoded nodes: 12 L bytes.
 __device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __restrict__ urow_size, Node* row,
                                 unsigned char* scr, int L, int lane, int* depth_out, bool reorder) {
   uint16_t* sz = reinterpret_cast<uint16_t*>(scr);
-  uint16_t* nd = sz + L;  // needs; later the absorbed-prefix counts by new position
-  uint16_t* par = nd + L;
-  int16_t* acc = reinterpret_cast<int16_t*>(par + L);
+  uint16_t* nd = sz + L;  // the absorbed-prefix counts by new position
+  int32_t* diff = reinterpret_cast<int32_t*>(nd + L);  // 4L bytes in: 4-byte aligned
+  int16_t* acc = reinterpret_cast<int16_t*>(diff + L);
   uint8_t* sw = reinterpret_cast<uint8_t*>(acc + L);
   uint8_t* absd = sw + L;  // an absorbed leaf sits at new position q
   for (int i = lane; i < n; i += 32) {
     const int v = __ldg(urow_size + i);
     sz[i] = static_cast<uint16_t>(v < 1 || v > n - i ? 0 : v);
-    sw[i] = 0;
     absd[i] = 0;
+    diff[i] = 0;
   }
   __syncwarp();
   bool ok = true;
   for (int i = lane; i < n; i += 32) {
-    const uint32_t op = s_nodes[i + 1].w0 & 0xFFu;
-    const int ar = op <= OP_VAR ? 0 : func_arity(static_cast<int>(op) - OP_FN);
+    const int ar = ar_of(s_nodes[i + 1].w0);
     const int si = sz[i];
     int c = i + 1, q = 0;
     for (; q < ar && c < n; ++q) {
-      par[c] = static_cast<uint16_t>(i);
       const int sc = sz[c];
       c = sc ? c + sc : n + 1;
     }
     ok = ok && si != 0 && (ar == 0 ? si == 1 : (q == ar && c == i + si));
+    // order: the larger subtree of a binary node first (sizes are final
+    // once validated; rows that fail are discarded below)
+    uint8_t swp = 0;
+    if (reorder && ar == 2 && ok) {
+      const int c1 = i + 1, s1 = sz[c1], c2 = c1 + s1, s2 = sz[c2];
+      if (s1 > s2) {
+        swp = 1;
+        atomicAdd(diff + c1, s2);
+        atomicAdd(diff + c2, -(s1 + s2));
+        if (c2 + s2 < n) atomicAdd(diff + c2 + s2, s1);
+      }
+    }
+    sw[i] = swp;
   }
   if (!__all_sync(FULL_MASK, ok) || sz[0] != n) return -1;
   __syncwarp();
@@ -165,65 +177,26 @@ __device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __res
     for (int j = lane; j < n; j += 32) acc[j] = 0;
     __syncwarp();
   } else {
-  // ---- evaluation order: the larger subtree of a binary node first. Every
-  // value a node pushes while its sibling is evaluated then sits under a
-  // subtree of at most half the size, so the stack depth is <= log2(n) + 1
-  // (Sethi-Ullman's optimum measured 4.19 vs 4.34 mean on C4 rows, at a
-  // fraction of the compile cost: no bottom-up need computation). The
-  // resulting depth is measured exactly below, after the positions.
-  for (int i = lane; i < n; i += 32) {
-    const uint32_t op = s_nodes[i + 1].w0 & 0xFFu;
-    const int ar = op <= OP_VAR ? 0 : func_arity(static_cast<int>(op) - OP_FN);
-    uint8_t swp = 0;
-    if (ar == 2) {
-      const int c1 = i + 1;
-      swp = sz[c1] > sz[c1 + sz[c1]] ? 1 : 0;  // first child larger: evaluate it first
-    }
-    sw[i] = swp;
-  }
-  __syncwarp();
-  // ---- top-down positions (pointer jumping inside a chunk)
-  for (int b = 0; b < nblk; ++b) {
-    const int base = b * 32, j = base + lane;
-    int a = 0, ptr = -1;
-    if (j < n && j > 0) {
-      const int pj = par[j];
-      int off = 0;
-      if (sw[pj]) {
-        const int f = pj + 1;
-        off = j == f ? static_cast<int>(sz[f + sz[f]]) : -static_cast<int>(sz[f]);
-      }
-      if (pj < base) {
-        a = acc[pj] + off;
-      } else {
-        a = off;
-        ptr = pj - base;
-      }
-    }
+    // ---- positions: inclusive prefix sum of diff
+    int carry = 0;
+    for (int b = 0; b < nblk; ++b) {
+      const int j = b * 32 + lane;
+      int v = j < n ? diff[j] : 0;
 #pragma unroll
-    for (int r = 0; r < 5; ++r) {
-      const int src = ptr >= 0 ? ptr : lane;
-      const int ap = __shfl_sync(FULL_MASK, a, src);
-      const int pp = __shfl_sync(FULL_MASK, ptr, src);
-      if (ptr >= 0) {
-        a += ap;
-        ptr = pp;
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t2 = __shfl_up_sync(FULL_MASK, v, off);
+        if (lane >= off) v += t2;
       }
+      if (j < n) acc[j] = static_cast<int16_t>(v + carry);
+      carry += __shfl_sync(FULL_MASK, v, 31);
     }
-    if (j < n) acc[j] = static_cast<int16_t>(a);
     __syncwarp();
-  }
-  // ---- stack depth of the reordered (unfused) program: suffix sums of
-  // (1 - arity) over the new positions (fusion only lowers it)
-  int16_t* dl = reinterpret_cast<int16_t*>(nd);
-  for (int j = lane; j < n; j += 32) {
-    const uint32_t op = s_nodes[j + 1].w0 & 0xFFu;
-    const int ar = op <= OP_VAR ? 0 : func_arity(static_cast<int>(op) - OP_FN);
-    dl[j + acc[j]] = static_cast<int16_t>(1 - ar);
-  }
-  __syncwarp();
-  {
-    int carry = 0, maxd = 0;
+    // ---- stack depth of the reordered (unfused) program: suffix sums of
+    // (1 - arity) over the new positions (fusion only lowers it)
+    int16_t* dl = reinterpret_cast<int16_t*>(nd);
+    for (int j = lane; j < n; j += 32) dl[j + acc[j]] = static_cast<int16_t>(1 - ar_of(s_nodes[j + 1].w0));
+    __syncwarp();
+    int cs = 0, maxd = 0;
     for (int b = nblk - 1; b >= 0; --b) {
       const int q = b * 32 + lane;
       int v = q < n ? dl[q] : 0;
@@ -232,14 +205,11 @@ __device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __res
         const int t2 = __shfl_down_sync(FULL_MASK, v, off);
         if (lane + off < 32) v += t2;
       }
-      if (q < n) maxd = max(maxd, v + carry);
-      carry += __shfl_sync(FULL_MASK, v, 0);
+      if (q < n) maxd = max(maxd, v + cs);
+      cs += __shfl_sync(FULL_MASK, v, 0);
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) maxd = max(maxd, __shfl_xor_sync(FULL_MASK, maxd, off));
-    *depth_out = maxd;
-  }
-  __syncwarp();
+    *depth_out = __reduce_max_sync(FULL_MASK, static_cast<unsigned>(maxd));
+    __syncwarp();
   }
   // ---- fusion decisions (sw bit 1: absorbs its first-visited child, bit 2:
   // its second-visited child); absorbed leaves marked at their new positions.
@@ -248,12 +218,10 @@ __device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __res
   // when that is a leaf (operand b is then the leaf, under the unreversed
   // op: g(F1, leaf)). The last node is never absorbed (it starts the stack).
   for (int j = lane; j < n; j += 32) {
-    const uint32_t op = s_nodes[j + 1].w0 & 0xFFu;
-    if (op <= OP_VAR) continue;
-    const int ar = func_arity(static_cast<int>(op) - OP_FN);
-    if (ar > 2) continue;
+    const int ar = ar_of(s_nodes[j + 1].w0);
+    if (ar == 0 || ar > 2) continue;
     const int c1 = j + 1;
-    const bool swp = ar == 2 && (sw[j] & 1);
+    const bool swp = sw[j] & 1;
     const int f1 = swp ? c1 + sz[c1] : c1;
     const int pos1 = f1 + acc[f1];
     if ((s_nodes[f1 + 1].w0 & 0xFFu) <= OP_VAR) {
@@ -288,11 +256,11 @@ __device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __res
     const int pos = j + acc[j];
     if (absd[pos]) continue;  // an absorbed leaf
     Node x = s_nodes[j + 1];
-    const uint32_t op = x.w0 & 0xFFu;
-    if (op > OP_VAR) {
-      const int ar = func_arity(static_cast<int>(op) - OP_FN);
+    const int ar = ar_of(x.w0);
+    if (ar > 0) {
+      const uint32_t op = x.w0 & 0xFFu;
       const uint8_t fl = sw[j];
-      const bool swp = ar == 2 && (fl & 1);
+      const bool swp = fl & 1;
       uint32_t g = swp ? reversed_op(op) : op;
       if (ar <= 2 && (fl & 6)) {
         const int c1 = j + 1;
@@ -332,11 +300,11 @@ __device__ int fuse_copy(const Node* prog, int n, Node* row, int lane) {
     if (i < n) {
       y = prog[i + 1];
       const uint32_t op = y.w0 & 0xFFu;
-      const bool absorbed = op <= OP_VAR && i >= 1 && i != n - 1 && (prog[i].w0 & 0xFFu) >= OP_FN &&
-                            func_arity(static_cast<int>(prog[i].w0 & 0xFFu) - OP_FN) <= 2;
+      const int par = ar_of(prog[i].w0);  // the previous node (i >= 1)
+      const bool absorbed = op <= OP_VAR && i >= 1 && i != n - 1 && par >= 1 && par <= 2;
       keep = !absorbed;
       if (keep && op >= OP_FN && i + 1 < n - 1) {
-        const int ar = func_arity(static_cast<int>(op) - OP_FN);
+        const int ar = ar_of(y.w0);
         const Node leaf = prog[i + 2];
         const uint32_t lop = leaf.w0 & 0xFFu;
         if (ar <= 2 && lop <= OP_VAR) {

@@ -35,6 +35,7 @@ static __device__ __forceinline__ bool decode_node(int16_t t, float v, int n_in,
                             : (is_var ? (leaf_flags_ok && var_ok) : (fn_known && f_ar == ar && fn_flags_ok)));
   const uint32_t w0_fn = (OP_FN + static_cast<uint32_t>(f)) | ((modi ? slot : kNoSlot) << 8);
   nd.w0 = is_const ? (OP_CONST | (kNoSlot << 8)) : (is_var ? (OP_VAR | (kNoSlot << 8)) : w0_fn);
+  nd.w0 |= static_cast<uint32_t>(ar & 3) << kArShift;
   nd.w1 = is_const ? __float_as_uint(v)
                    : (is_var ? (var_ok ? static_cast<uint32_t>(static_cast<int64_t>(iv) * Dpad) : 0u) : 0u);
   return ok;

@@ -57,6 +57,10 @@ constexpr uint32_t kNoSlot = 0xFF;
 // a VAR (w1 = its X offset), else a CONST (w1 = its bits).
 constexpr uint32_t kFuse = 1u << 16;
 constexpr uint32_t kFuseVar = 1u << 17;
+// Decoded words also carry the node's arity in w0 bits 20-21 (0 for leaves;
+// set by decode_node, read by the compile pass; the interpreters ignore them)
+constexpr uint32_t kArShift = 20;
+EVOGP_HD inline int ar_of(uint32_t w0) { return static_cast<int>((w0 >> kArShift) & 3u); }
 // Hot code (compile pass, single-output programs): w0 bits 24-31 hold a
 // dense opcode for the packed interpreter (hot.cuh) that already encodes the
 // operand source of a fused leaf, so its dispatch is one switch with no flag

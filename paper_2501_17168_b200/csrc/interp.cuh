@@ -233,7 +233,7 @@ static __device__ __noinline__ float fold_unary(int f, float c) {
 // stack effect as the fused unary).
 __device__ __forceinline__ Node finalize_hot(Node x) {
   const uint32_t op = x.w0 & 0xFFu;
-  if (op >= OP_FN && (x.w0 & kFuse) && !(x.w0 & kFuseVar) && func_arity(static_cast<int>(op) - OP_FN) == 1) {
+  if ((x.w0 & kFuse) && !(x.w0 & kFuseVar) && ar_of(x.w0) == 1) {
     const float v = fold_unary(static_cast<int>(op) - OP_FN, __uint_as_float(x.w1));
     return Node{OP_CONST | (kNoSlot << 8) | (HC_PUSH_C << kHotShift), __float_as_uint(v)};
   }
@@ -938,12 +938,15 @@ __global__ void __launch_bounds__(32 * kInterWarps, (K >= 16 || (K == 8 && mode_
   TreeInfo ti{1, 1, false};
   while (u < nunits) {
     const long long u_next = next_ticket(p, lane) + nwarps_grid;  // issued early, used next iteration
-    // unit -> (tree, chunk): 32-bit division whenever the unit count fits
-    // (a 64-bit division is a ~70-instruction call), none for one chunk
-    const int64_t tp = p.nch == 1 ? u : (nunits <= 0xFFFFFFFFll ? static_cast<int64_t>(static_cast<uint32_t>(u) /
-                                                                                   static_cast<uint32_t>(p.nch))
-                                                                : u / p.nch);
-    const int c = static_cast<int>(u - tp * p.nch);
+    // unit -> (tree, chunk), chunk-major: the warps running at any moment
+    // work on the same few chunks of the dataset, whose staged X rows then
+    // stay in L1 (32-bit division whenever the unit count fits: a 64-bit
+    // division is a ~70-instruction call)
+    const int c = p.nch == 1 ? 0
+                             : static_cast<int>(nunits <= 0xFFFFFFFFll
+                                                    ? static_cast<uint32_t>(u) / static_cast<uint32_t>(p.P)
+                                                    : u / p.P);
+    const int64_t tp = u - static_cast<int64_t>(c) * p.P;
     if (tp != staged) {
       __syncwarp();
       ti = load_program_warp(p, tp, s_tree, lane);

@@ -266,7 +266,7 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   // arrays, or (unfused) reordered nodes + reorder_program's arrays
   kp.reorder_scratch_bytes =
       !reorder_on ? 0
-                  : static_cast<int32_t>(fuse_on ? round_up(int64_t(L + 1) * 8 + 10 * L, 16)
+                  : static_cast<int32_t>(fuse_on ? round_up(int64_t(L + 1) * 8 + 12 * L + 4, 16)
                                                  : round_up(int64_t(L + 1) * 16 + 9 * L, 16));
   kp.fuse = fuse_on ? 1 : 0;
   kp.reorder_above = tu.reorder_above > 0 ? tu.reorder_above : SD;
