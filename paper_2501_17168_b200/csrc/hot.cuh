@@ -390,13 +390,15 @@ __device__ __forceinline__ bool interp_hot(const Node* __restrict__ tree, int le
   }
 // sin / cos: one range check per node; a warp whose points are all within
 // |x| <= 3 takes the reduction-free form (bit-identical there, fastmath.cuh)
-#define TRIG_BODY(APPROX)                                                               \
+#define TRIG_BODY(APPROX, EXT)                                                             \
   {                                                                                     \
     const float m = absmax<N2>(t);                                                      \
     if (__all_sync(FULL_MASK, m <= kSinCosSmall)) {                                     \
       FOR2 t[j] = pk(APPROX(lo(t[j])), APPROX(hi(t[j])));                               \
+    } else if (__any_sync(FULL_MASK, !(m <= kTrigReduceMax))) { /* rare: wide forms */ \
+      bail |= !(m <= kTrigWideMax) && !(absmax_noinf<N2>(t) <= kTrigWideMax);           \
+      FOR2 t[j] = pk(EXT(lo(t[j])), EXT(hi(t[j])));                                     \
     } else {                                                                            \
-      bail |= !(m <= kTrigReduceMax) && !(absmax_noinf<N2>(t) <= kTrigReduceMax);       \
       FOR2 {                                                                            \
         const u64 r = red2pi2(t[j]);                                                    \
         t[j] = pk(APPROX(lo(r)), APPROX(hi(r)));                                        \
@@ -408,8 +410,10 @@ __device__ __forceinline__ bool interp_hot(const Node* __restrict__ tree, int le
     const float m = absmax<N2>(t);                                                      \
     if (__all_sync(FULL_MASK, m <= kTanSmall)) {                                        \
       FOR2 t[j] = poly_tan2(t[j]);                                                      \
+    } else if (__any_sync(FULL_MASK, !(m <= kTrigReduceMax))) { /* rare: wide forms */ \
+      bail |= !(m <= kTrigWideMax) && !(absmax_noinf<N2>(t) <= kTrigWideMax);           \
+      FOR2 t[j] = pk(fm_tan_ext(lo(t[j])), fm_tan_ext(hi(t[j])));                       \
     } else {                                                                            \
-      bail |= !(m <= kTrigReduceMax) && !(absmax_noinf<N2>(t) <= kTrigReduceMax);       \
       FOR2 t[j] = tan_full2(t[j]);                                                      \
     }                                                                                   \
   }
@@ -450,8 +454,8 @@ __device__ __forceinline__ bool interp_hot(const Node* __restrict__ tree, int le
       BIN_CASES(HC_SUBR, sub2(b2, a2))
       DIV_CASES(HC_DIV, t, b)
       DIV_CASES(HC_DIVR, b, t)
-      UN_CASES(HC_SIN, TRIG_BODY(sin_ap))
-      UN_CASES(HC_COS, TRIG_BODY(cos_ap))
+      UN_CASES(HC_SIN, TRIG_BODY(sin_ap, fm_sin_ext))
+      UN_CASES(HC_COS, TRIG_BODY(cos_ap, fm_cos_ext))
       UN_CASES(HC_TAN, TAN_BODY)
       default:
         if constexpr (PAPER) {

@@ -547,9 +547,18 @@ def test_fast_trig_accuracy():
     assumes (R14): |err| <= ABS + ulps * ulp(|ref|)."""
     rng = np.random.default_rng(11)
     near = (np.arange(-2000, 2001)[:, None] * (np.pi / 2) + rng.uniform(-1e-3, 1e-3, (4001, 64))).ravel()
+    # the wide forms (FP64 reduction, 105615 < |x| <= 2^40): log-uniform
+    # magnitudes and FP32 values nearest to multiples of pi/2 (tan's poles and
+    # zeros; the FP32 grid keeps them >= ~2^-30 away) up to 2^30
+    wide = np.sign(rng.standard_normal(1 << 18)) * np.exp2(rng.uniform(np.log2(1e5), 40, 1 << 18))
+    kk = np.exp2(rng.uniform(16, 30, 1 << 16)).astype(np.int64)
+    near_w = (kk * (np.pi / 2)).astype(np.float32).astype(np.float64)
+    near_w = np.concatenate([near_w, np.nextafter(near_w.astype(np.float32), np.float32(np.inf)).astype(np.float64)])
     xs = np.concatenate([rng.uniform(-10, 10, 1 << 20), rng.uniform(-1e5, 1e5, 1 << 19),
                          np.sign(rng.standard_normal(1 << 18)) * 10 ** rng.uniform(-8, 0, 1 << 18), near,
-                         rng.uniform(1e5, 1e7, 4096), np.array([0.0, -0.0, 1e30, -1e30])]).astype(np.float32)
+                         rng.uniform(1e5, 1e7, 4096), wide, near_w,
+                         np.array([0.0, -0.0, 1e30, -1e30, 105615.0, 105616.0, 2.0 ** 40, -(2.0 ** 40), 1.2e12])
+                         ]).astype(np.float32)
     pt = synth.PrefixTrees(np.array([0, 2, 4, 6], np.int64), np.array([2, 1, 2, 1, 2, 1], np.int16),
                            np.array([4, 0, 5, 0, 6, 0], np.float32))
     dt = to_device(pt, 2, 1)
@@ -567,6 +576,31 @@ def test_fast_trig_accuracy():
 
 
 TRIG_ABS = 2.0 ** -20  # absolute error budget of sin.approx / cos.approx on [-pi, pi] (measured, R14)
+
+
+def test_trig_wide_hot_equals_cold():
+    """A point's sin / cos / tan value does not depend on which interpreter
+    copy ran: the same arguments (105615 < |x| <= 2^40, the wide forms, and
+    the FP32 range) once in chunks that stay hot and once in chunks that
+    re-run cold (one x1 = 1e30 per chunk sends the chunk to the library
+    copy, whose result is multiplied by zero)."""
+    rng = np.random.default_rng(12)
+    n = 1 << 16
+    x0 = np.concatenate([np.sign(rng.standard_normal(n)) * np.exp2(rng.uniform(0, 40, n)),
+                         rng.uniform(-4, 4, 1024)]).astype(np.float32)
+    # f(x0) + 0 * sin(x1): ADD, f, x0, MUL, 0, SIN, x1   (f = sin, cos, tan)
+    pt = synth.PrefixTrees(np.array([0, 7, 14, 21], np.int64),
+                           np.array([3, 2, 1, 3, 0, 2, 1] * 3, np.int16),
+                           np.array([v for f in (4, 5, 6) for v in (0, f, 0, 2, 0, 4, 1)], np.float32))
+    dt = to_device(pt, 7, 2)
+    hot = np.stack([x0, np.ones_like(x0)], axis=1)
+    cold = hot.copy()
+    cold[::32, 1] = 1e30  # one per 32 points: every chunk of every kernel re-runs cold
+    for strategy in ("inter", "intra"):
+        gh = gpu_eval(dt, hot, 1, strategy)[:, :, 0]
+        gc = gpu_eval(dt, cold, 1, strategy)[:, :, 0]
+        ok = (gh == gc) | (np.isnan(gh) & np.isnan(gc))
+        assert ok.all(), (strategy, (~ok).sum(), x0[np.nonzero(~ok)[1][:4]])
 
 
 def test_ieee_fast_paths_bitexact():
