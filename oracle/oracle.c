@@ -333,7 +333,8 @@ static double cert_f(int f, const double* a, const double* e, double r, int* rob
    * on [-pi, pi] by 2^-21.41 / 2^-21.19 absolute; an exhaustive B200 sweep of
    * every FP32 argument in [-pi, pi] measured 2^-21.46 / 2^-21.24
    * (tests/test_gpu_accuracy.py). The budget 2^-20 adds room for the
-   * reduction's own error at |x| up to 105615 (R14). */
+   * reduction's own error (FP32 split to |x| <= 105615, FP64 split to
+   * 2^40; R14). */
   if (f == F_SIN || f == F_COS) out += SFU_TRIG_ABS;
   if (isnan(out)) out = INFINITY;
   return out;
