@@ -6,6 +6,8 @@ rows = ["| Config | value (GPops/s) | strategy | kernel (GPops/s) | roof frac | 
         "|---|---|---|---|---|---|---|---|"]
 for c in ("c3", "c2", "c4", "c5", "c1", "g1", "n2"):
     p = os.path.join(src, f"bench_{c}.json") if os.path.isdir(src) else f"gpurun_out/bench_{c}_{src}.json"
+    if os.path.isdir(src) and not os.path.exists(p):
+        p = os.path.join(src, f"{c}.json")
     if not os.path.exists(p):
         continue
     d = json.load(open(p))
