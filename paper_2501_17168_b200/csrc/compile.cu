@@ -411,20 +411,25 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
   }
 }
 
-// a7 combine: res[t] = (sum over the tree's units of their partials, in unit
-// order) [/ D]. One thread per tree; launched after the evaluation kernel
-// when a tree spans several units.
+// a7 combine: res[t] = (sum of the tree's per-unit partials) [/ D], one warp
+// per tree in a fixed order (lane l sums units l, l + 32, ... in turn, then a
+// fixed shuffle tree), so the result is deterministic (reading R9); launched
+// after the evaluation kernel when a tree spans several units (kernel (a) on a
+// large D has thousands of units per tree).
 __global__ void __launch_bounds__(256) k_combine(const KParams p) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (t >= p.P) return;
   const double* q = p.partials + t * p.nparts;
   double acc = 0.0;
-  for (int i = 0; i < p.nparts; ++i) acc += q[i];
-  p.res[t] = p.div_by_D ? acc / static_cast<double>(p.D) : acc;
+  for (int i = lane; i < p.nparts; i += 32) acc += q[i];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, off);
+  if (lane == 0) p.res[t] = p.div_by_D ? acc / static_cast<double>(p.D) : acc;
 }
 
 void launch_combine(const KParams& kp, cudaStream_t s) {
-  const int64_t blocks = (kp.P + 255) / 256;
+  const int64_t blocks = (kp.P + 7) / 8;
   k_combine<<<static_cast<int>(blocks), 256, 0, s>>>(kp);
 }
 
