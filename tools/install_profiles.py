@@ -32,16 +32,18 @@ def launch_stats(path):
             for k, v in per.items() if "evogp" in k}
 
 
-names = {"c2": "ncu_c2_inter_summary.json", "c3": "ncu_c3_intra_summary.json", "c4": "ncu_c4_inter_summary.json",
-         "c5": "ncu_c5_intra_summary.json", "n2": "ncu_n2_paired_summary.json"}
-for c, out in names.items():
+names = {}
+for c in ["c2", "c3", "c4", "c5", "n2"]:
+    # named after the kernel the capture holds (the selector's choice), as bench.py looks it up
     d = json.load(open(f"{R}/prof_{c}_{TAG}.json"))
+    kind = "paired" if "k_paired" in d["kernel"] else ("intra" if "k_intra" in d["kernel"] else "inter")
+    out = names[c] = f"ncu_{c}_{kind}_summary.json"
     d["note"] = f"refresh {TAG}: bench.py --config {c}"
     d["launch_list"] = launch_stats(f"gpurun_out/launches_{c}_{TAG}.csv")
     json.dump(d, open("profiles/" + out, "w"), indent=1)
     shutil.copy(f"gpurun_out/launches_{c}_{TAG}.csv", f"profiles/launches_{c}_{TAG}.csv")
     shutil.copy(f"{R}/prof_{c}_{TAG}.sass.csv.gz", f"profiles/sass_{c}_{TAG}.csv.gz")
-for k in ["k_inter", "k_prepare", "k_reproduce"]:
+for k in ["k_eval", "k_prepare", "k_reproduce"]:
     d = json.load(open(f"{R}/prof_g1_{k}_{TAG}.json"))
     d["note"] = f"refresh {TAG}: bench.py --config g1 --warmup 20 (populations grown by 20 generations)"
     d["launch_list"] = launch_stats(f"gpurun_out/launches_g1_{TAG}.csv")
