@@ -76,7 +76,7 @@ int run(int mode, const int16_t* type, const float* value, const int16_t* size, 
   kp.res = res;
   kp.div_by_D = div_by_D;
   kp.ctl = reinterpret_cast<Control*>(ws + pl.off_ctl);
-  kp.counters = reinterpret_cast<int32_t*>(ws + pl.off_counters);
+  kp.long_rows = reinterpret_cast<int32_t*>(ws + pl.off_long);
   kp.partials = reinterpret_cast<double*>(ws + pl.off_partials);
   kp.deep_locks = reinterpret_cast<int32_t*>(ws + pl.off_locks);
   kp.deep = reinterpret_cast<float*>(ws + pl.off_deep);

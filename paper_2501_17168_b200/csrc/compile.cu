@@ -323,15 +323,68 @@ __device__ int fuse_copy(const Node* prog, int n, Node* row, int lane) {
   return carry;
 }
 
+// Compile one row with the whole warp (decode / validate, reorder when deeper
+// than the evaluation kernel's shared stack, fuse leaves, hot codes), using
+// `scratch` sized for rows of up to Lc nodes (the row is at most that long).
+__device__ void compile_row_warp(const KParams& p, int64_t tp, unsigned char* scratch, int Lc, int lane) {
+  Node* row = p.prog + tp * p.prog_ld;
+  TreeInfo ti;
+  if (p.reorder_scratch_bytes > 0) {
+    // decode into shared scratch; reorder when the row is deeper than the
+    // evaluation kernel's shared stack; then fuse leaves while copying out
+    Node* s_nodes = reinterpret_cast<Node*>(scratch);
+    Node* s_reord = s_nodes + (Lc + 1);
+    ti = stage_tree_warp(p, tp, s_nodes, lane);
+    const Node* prog = s_nodes;
+    if (ti.valid && p.fuse && ti.maxdepth - 1 > p.reorder_above) {
+      // warp-parallel reorder + fusion straight into the program row; rows
+      // with inconsistent caller sizes take fuse_copy (no reordering). Rows
+      // that need no reordering also take fuse_copy: the second-child fusion
+      // of reorder_fuse_par(reorder = false) measured +1-2% in the kernels
+      // but -5% on c4's whole step (the compile pass costs more than it saves)
+      int dep = ti.maxdepth;
+      const int len = reorder_fuse_par(s_nodes, ti.len, p.size + tp * p.ld, row, scratch + (Lc + 1) * 8, Lc,
+                                       lane, &dep, true);
+      if (len > 0) {
+        ti.len = len;
+        ti.maxdepth = dep;
+        goto compiled;
+      }
+    } else if (ti.valid && ti.maxdepth - 1 > p.reorder_above) {
+      {
+        ti.maxdepth = reorder_program(s_nodes, ti.len, s_reord, scratch + 2 * (Lc + 1) * 8, Lc, lane);
+        prog = s_reord;
+      }
+    }
+    if (ti.valid && p.fuse) {
+      ti.len = fuse_copy(prog, ti.len, row, lane);
+    } else {
+      for (int i = lane; i <= ti.len; i += 32) {
+        const Node x = prog[i];
+        row[i] = i == 0 ? x : finalize_hot(x);
+      }
+      __syncwarp();
+    }
+  } else {
+    ti = stage_tree_warp(p, tp, row, lane, true);  // hot codes (multi-output rows: + Modi twins)
+  }
+compiled:
+  if (lane == 0) {
+    p.info[tp] = TreeMeta{ti.len, ti.valid ? (ti.maxdepth | (ti.paper ? kPaperRow : 0)) : -1};
+    if (!ti.valid) atomicOr(&p.ctl->flags, 1);
+  }
+  __syncwarp();
+}
+
 // ------------------------------------------------------------------------
 // a2 + a4 (compile): one launch before the evaluation kernel
 //   * X (row-major or SoA) -> padded SoA rows Xs[n_in][Dpad] (+ y for the SSE)
 //   * every tree row -> its decoded program row (one warp per tree): decode,
 //     validate, stack depth; so the evaluation kernels only copy programs
-//   * clears the per-tree completion counters and the work-queue tickets
+//   * clears the work-queue tickets
 // ------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* __restrict__ X, int32_t x_layout,
-                                                 const float* __restrict__ y, int y_is_label, int64_t n_counters) {
+                                                 const float* __restrict__ y, int y_is_label) {
   const int64_t rows = p.n_in + (y ? 1 : 0);
   const int64_t total = rows * p.Dpad;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -346,7 +399,6 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
     }
     xs[e] = v;
   }
-  for (int64_t e = t0; e < n_counters; e += stride) p.counters[e] = 0;
   // the deep-pool locks are re-zeroed every call: a workspace may be reused
   // across plans whose section offsets differ (e.g. inter vs intra partials)
   for (int64_t e = t0; e < p.deep_slots; e += stride) p.deep_locks[e] = 0;
@@ -361,54 +413,46 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* scratch = smem + static_cast<size_t>(threadIdx.x >> 5) * p.reorder_scratch_bytes;
   for (int64_t tp = t0 >> 5; tp < p.P; tp += nwarps) {
-    Node* row = p.prog + tp * p.prog_ld;
-    TreeInfo ti;
-    if (p.reorder_scratch_bytes > 0) {
-      // decode into shared scratch; reorder when the row is deeper than the
-      // evaluation kernel's shared stack; then fuse leaves while copying out
-      Node* s_nodes = reinterpret_cast<Node*>(scratch);
-      Node* s_reord = s_nodes + (p.L + 1);
-      ti = stage_tree_warp(p, tp, s_nodes, lane);
-      const Node* prog = s_nodes;
-      if (ti.valid && p.fuse && ti.maxdepth - 1 > p.reorder_above) {
-        // warp-parallel reorder + fusion straight into the program row; rows
-        // with inconsistent caller sizes take fuse_copy (no reordering). Rows
-        // that need no reordering also take fuse_copy: the second-child fusion
-        // of reorder_fuse_par(reorder = false) measured +1-2% in the kernels
-        // but -5% on c4's whole step (the compile pass costs more than it saves)
-        int dep = ti.maxdepth;
-        const int len = reorder_fuse_par(s_nodes, ti.len, p.size + tp * p.ld, row, scratch + (p.L + 1) * 8, p.L,
-                                         lane, &dep, true);
-        if (len > 0) {
-          ti.len = len;
-          ti.maxdepth = dep;
-          goto compiled;
-        }
-      } else if (ti.valid && ti.maxdepth - 1 > p.reorder_above) {
-        {
-          ti.maxdepth = reorder_program(s_nodes, ti.len, s_reord, scratch + 2 * (p.L + 1) * 8, p.L, lane);
-          prog = s_reord;
-        }
+    if (p.prep_cap < p.L) {
+      // the long tier: rows longer than this kernel's scratch are queued (as
+      // are malformed lengths, which the long tier flags)
+      const int len0 = __ldg(p.size + tp * p.ld);
+      if (len0 > p.prep_cap) {
+        if (lane == 0) p.long_rows[atomicAdd(&p.ctl->nlong, 1u)] = static_cast<int32_t>(tp);
+        continue;
       }
-      if (ti.valid && p.fuse) {
-        ti.len = fuse_copy(prog, ti.len, row, lane);
-      } else {
-        for (int i = lane; i <= ti.len; i += 32) {
-          const Node x = prog[i];
-          row[i] = i == 0 ? x : finalize_hot(x);
-        }
-        __syncwarp();
-      }
-    } else {
-      ti = stage_tree_warp(p, tp, row, lane, true);  // hot codes (multi-output rows: + Modi twins)
     }
-  compiled:
-    if (lane == 0) {
-      p.info[tp] = TreeMeta{ti.len, ti.valid ? (ti.maxdepth | (ti.paper ? kPaperRow : 0)) : -1};
-      if (!ti.valid) atomicOr(&p.ctl->flags, 1);
-    }
-    __syncwarp();
+    compile_row_warp(p, tp, scratch, p.prep_cap, lane);
   }
+}
+
+// The long tier: rows queued by k_prepare (longer than its scratch), one warp
+// per row with scratch sized for max_len.
+__global__ void __launch_bounds__(256) k_prepare_long(const KParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  unsigned char* scratch = smem + static_cast<size_t>(threadIdx.x >> 5) * p.long_scratch_bytes;
+  const uint32_t n = p.ctl->nlong;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < n; i += nwarps)
+    compile_row_warp(p, p.long_rows[i], scratch, p.L, lane);
+}
+
+void launch_prepare_long(const KParams& kp, cudaStream_t s) {
+  const int wpb = std::max(1, std::min(8, (220 * 1024) / std::max(kp.long_scratch_bytes, 1)));
+  const size_t psmem = static_cast<size_t>(wpb) * kp.long_scratch_bytes;
+  if (psmem > 48 * 1024) {
+    static thread_local int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+      cudaFuncSetAttribute(k_prepare_long, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      attr_dev = dev;
+    }
+  }
+  // a persistent grid over the queue (its length is known only on the device)
+  const int64_t blocks = static_cast<int64_t>(kp.sms) * std::max(1, 8 / wpb) * 2;
+  k_prepare_long<<<static_cast<int>(blocks), 32 * wpb, psmem, s>>>(kp);
 }
 
 // a7 combine: res[t] = (sum of the tree's per-unit partials) [/ D], one warp
@@ -457,7 +501,7 @@ void launch_prepare(const KParams& kp, int mode, const float* X, int32_t x_layou
       1, std::min<int64_t>(std::max((total + threads - 1) / threads, (kp.P + wpb - 1) / wpb),
                            static_cast<int64_t>(kp.sms) * 16 * (8 / wpb)));
   k_prepare<<<static_cast<int>(blocks), threads, psmem, s>>>(kp, X, x_layout, mode_reduce(mode) ? y : nullptr,
-                                                            mode == MODE_CLS, 0);
+                                                            mode == MODE_CLS);
 }
 
 }  // namespace evogp

@@ -133,6 +133,8 @@ struct Control {
   uint32_t cold_chunks;     // chunks re-run on the cold interpreter copy (diagnostic, per call)
   unsigned long long work;  // dynamic work-queue ticket counter (zeroed by k_stage_x)
   unsigned long long deep;  // deep-stack pool ticket counter
+  uint32_t nlong;           // rows queued for k_prepare_long (zeroed before k_prepare when it runs)
+  uint32_t pad_;
 };
 
 // Everything a kernel launch needs; built by plan_problem() on the host.
@@ -170,8 +172,14 @@ struct KParams {
   int32_t reorder_scratch_bytes;  // k_prepare shared scratch per warp (0: no reordering / fusion)
   int32_t fuse;                   // leaf fusion on (single-output programs with scratch)
   int32_t reorder_above;          // rows with maxdepth - 1 > this are reordered
+  // two-tier compile: k_prepare's per-warp scratch (reorder_scratch_bytes) is
+  // sized for rows of up to prep_cap nodes; longer rows are queued and
+  // compiled by k_prepare_long with long_scratch_bytes per warp (prep_cap == L:
+  // one tier)
+  int32_t prep_cap;
+  int32_t long_scratch_bytes;
   double* partials;
-  int32_t* counters;
+  int32_t* long_rows;  // rows longer than prep_cap, compiled by k_prepare_long (P slots)
   Control* ctl;
   int32_t* deep_locks;
   float* deep;
@@ -189,7 +197,7 @@ struct Plan {
   size_t smem_bytes;
   KParams kp;
   // workspace layout
-  size_t off_ctl, off_xs, off_counters, off_partials, off_locks, off_deep, off_deep_pw, off_prog, off_info, total;
+  size_t off_ctl, off_xs, off_long, off_partials, off_locks, off_deep, off_deep_pw, off_prog, off_info, total;
 };
 
 // kernels.cu
@@ -204,6 +212,7 @@ const evogp_tuning& tuning();
 // compile.cu
 void launch_prepare(const KParams& kp, int mode, const float* X, int32_t x_layout, const float* y,
                     cudaStream_t s);
+void launch_prepare_long(const KParams& kp, cudaStream_t s);
 void launch_combine(const KParams& kp, cudaStream_t s);
 
 // eval_*.cu: the instantiated evaluation kernels for one (strategy, K), by mode

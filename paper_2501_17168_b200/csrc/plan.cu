@@ -46,6 +46,8 @@ constexpr int kReorderMaxLen = kMaxLenSupported;
 // levels of the per-warp private global stacks (rows deeper than every
 // shared-memory pass split and than this fall back to the locked pool)
 constexpr int kDeepPerWarpLevels = 32;
+// k_prepare's row-length tier (two-tier compile when max_len > 2 * kPrepCap)
+constexpr int kPrepCap = 192;
 
 // instantiated kernels (eval_*.cu): single-output modes at every K the plan
 // uses, multi-output (Modi) modes at K <= 4 (the plan never gives them K = 8)
@@ -264,10 +266,20 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   const bool fuse_on = reorder_on && tu.no_fuse == 0;  // leaf fusion of single-output programs
   // shared scratch per compiling warp: decoded nodes + reorder_fuse_par's
   // arrays, or (unfused) reordered nodes + reorder_program's arrays
-  kp.reorder_scratch_bytes =
-      !reorder_on ? 0
-                  : static_cast<int32_t>(fuse_on ? round_up(int64_t(L + 1) * 8 + 12 * L + 4, 16)
-                                                 : round_up(int64_t(L + 1) * 16 + 9 * L, 16));
+  // per-warp scratch for rows of up to Lc nodes: decoded nodes + reorder_fuse_par's arrays,
+  // or (unfused) reordered nodes + reorder_program's arrays
+  auto scratch_for = [&](int64_t Lc) -> int32_t {
+    return !reorder_on ? 0
+                       : static_cast<int32_t>(fuse_on ? round_up(int64_t(Lc + 1) * 8 + 12 * Lc + 4, 16)
+                                                      : round_up(int64_t(Lc + 1) * 16 + 9 * Lc, 16));
+  };
+  // two tiers for long max_len (evolved populations are mostly far shorter
+  // than max_len, and scratch sized for max_len caps k_prepare at 2 CTAs per
+  // SM at L = 512: 30% issue on g1): rows of up to kPrepCap nodes in
+  // k_prepare, longer ones queued for k_prepare_long
+  kp.prep_cap = (reorder_on && L > 2 * kPrepCap) ? kPrepCap : L;
+  kp.reorder_scratch_bytes = scratch_for(kp.prep_cap);
+  kp.long_scratch_bytes = kp.prep_cap < L ? scratch_for(L) : 0;
   kp.fuse = fuse_on ? 1 : 0;
   kp.reorder_above = tu.reorder_above > 0 ? tu.reorder_above : SD;
   kp.out_magic = static_cast<int32_t>((0x100000000ull + n_out - 1) / n_out);
@@ -280,7 +292,7 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   off += 256;
   pl.off_xs = off;
   off += round_up(static_cast<int64_t>(n_in + 1) * Dpad * 4, 256);
-  pl.off_counters = off;
+  pl.off_long = off;
   off += round_up(P * 4, 256);
   pl.off_partials = off;
   off += mode_reduce(mode) && kp.nparts > 1 ? round_up(P * kp.nparts * 8, 256) : 0;
@@ -304,8 +316,13 @@ int launch(Plan& pl, int mode, const float* X, int32_t x_layout, const float* y,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   KParams& kp = pl.kp;
   int launches = 0;
+  if (kp.prep_cap < kp.L) cudaMemsetAsync(&kp.ctl->nlong, 0, sizeof(uint32_t), s);
   launch_prepare(kp, mode, X, x_layout, y, s);  // a2 + a4 (compile.cu)
   ++launches;
+  if (kp.prep_cap < kp.L) {  // the long rows' tier
+    launch_prepare_long(kp, s);
+    ++launches;
+  }
   const void* fn = kernel_ptr(pl.strategy, pl.K, mode);
   if (!fn) return EVOGP_E_ARG;
   void* args[] = {&kp};

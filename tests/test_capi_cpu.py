@@ -128,9 +128,12 @@ def test_too_large_and_empty():
 def test_workspace_and_selector_host():
     assert evogp.workspace_size(10_000, 1024, 63, 4, 1) > 4 * 1024 * 4
     assert evogp.workspace_size(1000, 1 << 20, 127, 8, 1) >= 8 * (1 << 20) * 4
-    # small D -> hybrid (inter), large D -> data-level (intra)
+    # the measured table (selector_table.json, profiles/selector_calibration_r02d.log):
+    # cells whose faster kernel wins by >= 30% on both calibration passes
     assert evogp.select_strategy(10_000, 1024, 63) == "inter"
-    assert evogp.select_strategy(1000, 1 << 20, 127) == "intra"
+    assert evogp.select_strategy(1_000_000, 256, 127) == "inter"
+    assert evogp.select_strategy(1000, 65536, 512) == "intra"
+    assert evogp.select_strategy(10_000, 4096, 512) == "intra"
 
 
 def test_gp_config_struct_layout_matches_header(tmp_path):

@@ -470,23 +470,24 @@ def _subset(pt, rows):
     return np.array(offs, np.int64), np.concatenate(tys), np.concatenate(vas)
 
 
-def _c3_device_eval(pt, cfg, rows):
-    """Full C3 population on the device in the bench's launch configuration
-    (strategy auto -> kernel (b)); returns the sampled rows' outputs."""
+def _c3_device_eval(pt, cfg, rows, strategy):
+    """Full C3 population on the device with kernel `strategy` (the bench's
+    launch configuration is strategy auto, which the measured table resolves
+    to one of the two); returns the sampled rows' outputs."""
     evogp = _evogp()
     t, v, s = to_device(pt, cfg.max_len, cfg.n_in)
     X, y = synth.config_data(cfg)
     Xd = torch.from_numpy(X).cuda()
-    assert evogp.select_strategy(cfg.P, cfg.D, cfg.max_len) == "intra"
-    out = evogp.eval(t, v, s, Xd)  # [P, 2^20, 1]
+    out = evogp.eval(t, v, s, Xd, strategy=strategy)  # [P, 2^20, 1]
     g = out[torch.from_numpy(rows).cuda(), :, 0].cpu().numpy()
-    m = evogp.sr_fitness(t, v, s, Xd, torch.from_numpy(y).cuda()).cpu().numpy()
+    m = evogp.sr_fitness(t, v, s, Xd, torch.from_numpy(y).cuda(), strategy=strategy).cpu().numpy()
     del out
     torch.cuda.empty_cache()
     return g, m, X, y
 
 
-def test_full_size_c3_ieee_bitexact():
+@pytest.mark.parametrize("strategy", ["inter", "intra"])
+def test_full_size_c3_ieee_bitexact(strategy):
     """C3 at full size (P=1000, L=127, n_in=8, D=2^20, PAPER P:354's
     data-parallel regime): on the IEEE-exact mix, 16 sampled trees over all
     2^20 points are bit-identical to the FP32-faithful oracle, and their fused
@@ -494,7 +495,7 @@ def test_full_size_c3_ieee_bitexact():
     cfg = synth.CONFIGS["c3"]
     pt = synth.config_trees(cfg, synth.M_IEEE)
     rows = _sample_rows(cfg.P, 16, seed=3)
-    g, m, X, y = _c3_device_eval(pt, cfg, rows)
+    g, m, X, y = _c3_device_eval(pt, cfg, rows, strategy)
     sub = synth.PrefixTrees(*_subset(pt, rows))
     ot, ov, osz = oracle_arrays(sub, cfg.max_len, cfg.n_in)
     r32 = oracle.evaluate(ot, ov, osz, X, mode=1)[:, :, 0]
@@ -507,7 +508,8 @@ def test_full_size_c3_ieee_bitexact():
     assert (np.abs(m[rows][fin] - ref[fin]) <= 1e-10 * np.abs(ref[fin])).all()
 
 
-def test_full_size_c3_paper_certified():
+@pytest.mark.parametrize("strategy", ["inter", "intra"])
+def test_full_size_c3_paper_certified(strategy):
     """C3 at full size on the paper mix (the bench's headline workload): every
     certified point of 16 sampled trees (all 2^20 points each) within the
     north-star tolerance with identical class, every MSE-certified tree within
@@ -515,7 +517,7 @@ def test_full_size_c3_paper_certified():
     cfg = synth.CONFIGS["c3"]
     pt = synth.config_trees(cfg, synth.M_PAPER)
     rows = _sample_rows(cfg.P, 16, seed=3)
-    g, m, X, y = _c3_device_eval(pt, cfg, rows)
+    g, m, X, y = _c3_device_eval(pt, cfg, rows, strategy)
     sub = synth.PrefixTrees(*_subset(pt, rows))
     ot, ov, osz = oracle_arrays(sub, cfg.max_len, cfg.n_in)
     r64, e, rob = oracle.evaluate(ot, ov, osz, X, mode=0, certify=True)
