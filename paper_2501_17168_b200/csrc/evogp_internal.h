@@ -155,6 +155,8 @@ struct KParams {
   double* res;      // mse or sse
   int32_t div_by_D; // 1: mse, 0: sse
   int32_t nch;      // chunks of 32*K points per tree
+  int32_t ucs;      // inter: chunks per work unit
+  int32_t ngrp;     // inter: work units (chunk groups) per tree, ceil(nch / ucs)
   int32_t nparts;   // partial sums per tree (inter: nch, intra: nseg)
   int32_t nseg;     // intra: segments per tree
   int32_t seg_chunks;

@@ -929,7 +929,7 @@ __global__ void __launch_bounds__(32 * kInterWarps, (K >= 16 || (K == 8 && mode_
   Node* s_tree = reinterpret_cast<Node*>(wbase);
   float* s_stack_l = reinterpret_cast<float*>(wbase + p.tree_bytes) + lane * V;
   float* s_acc_l = s_stack_l + p.SD * 32 * K;
-  const long long nunits = p.P * p.nch;
+  const long long nunits = p.P * p.ngrp;
   // first unit: the warp's global index (no atomic); then the shared queue,
   // whose tickets start after the grid's warps
   const long long nwarps_grid = static_cast<long long>(gridDim.x) * kInterWarps;
@@ -938,34 +938,39 @@ __global__ void __launch_bounds__(32 * kInterWarps, (K >= 16 || (K == 8 && mode_
   TreeInfo ti{1, 1, false};
   while (u < nunits) {
     const long long u_next = next_ticket(p, lane) + nwarps_grid;  // issued early, used next iteration
-    // unit -> (tree, chunk), chunk-major: the warps running at any moment
-    // work on the same few chunks of the dataset, whose staged X rows then
-    // stay in L1 (32-bit division whenever the unit count fits: a 64-bit
+    // unit -> (tree, chunk group), chunk-major: the warps running at any
+    // moment work on the same few chunks of the dataset, whose staged X rows
+    // then stay in L1 (32-bit division whenever the unit count fits: a 64-bit
     // division is a ~70-instruction call)
-    const int c = p.nch == 1 ? 0
-                             : static_cast<int>(nunits <= 0xFFFFFFFFll
-                                                    ? static_cast<uint32_t>(u) / static_cast<uint32_t>(p.P)
-                                                    : u / p.P);
-    const int64_t tp = u - static_cast<int64_t>(c) * p.P;
+    const int g = p.ngrp == 1 ? 0
+                              : static_cast<int>(nunits <= 0xFFFFFFFFll
+                                                     ? static_cast<uint32_t>(u) / static_cast<uint32_t>(p.P)
+                                                     : u / p.P);
+    const int64_t tp = u - static_cast<int64_t>(g) * p.P;
     if (tp != staged) {
       __syncwarp();
       ti = load_program_warp(p, tp, s_tree, lane);
       staged = tp;
     }
-    const int64_t chunk_base = static_cast<int64_t>(c) * (32 * K);
-    float tos[K];
-    if (mode_multi(MODE) && !ti.valid) zero_acc<K>(s_acc_l, p.n_out);
-    if (ti.valid) run_chunk<K, mode_multi(MODE)>(p, s_tree, ti, chunk_base, lane, s_stack_l, s_acc_l, tos);
-    if (MODE == MODE_EVAL1) {
-      store_out1<K>(p, tp, chunk_base, lane, tos, ti.valid);
-    } else if (MODE == MODE_EVALN) {
-      store_outn<K>(p, tp, chunk_base, lane, s_acc_l - lane * V, ti.valid);
-    } else {
-      double s = !ti.valid ? kNaN64
-                           : (MODE == MODE_CLS ? lane_correct<K>(p, chunk_base, lane, s_acc_l - lane * V)
-                                               : lane_sse<K>(p, chunk_base, lane, tos));
+    const int c0 = g * p.ucs, c1 = min(p.nch, c0 + p.ucs);
+    double s = 0.0;
+    for (int c = c0; c < c1; ++c) {
+      const int64_t chunk_base = static_cast<int64_t>(c) * (32 * K);
+      float tos[K];
+      if (mode_multi(MODE) && !ti.valid) zero_acc<K>(s_acc_l, p.n_out);
+      if (ti.valid) run_chunk<K, mode_multi(MODE)>(p, s_tree, ti, chunk_base, lane, s_stack_l, s_acc_l, tos);
+      if (MODE == MODE_EVAL1) {
+        store_out1<K>(p, tp, chunk_base, lane, tos, ti.valid);
+      } else if (MODE == MODE_EVALN) {
+        store_outn<K>(p, tp, chunk_base, lane, s_acc_l - lane * V, ti.valid);
+      } else if (ti.valid) {
+        s += MODE == MODE_CLS ? lane_correct<K>(p, chunk_base, lane, s_acc_l - lane * V)
+                              : lane_sse<K>(p, chunk_base, lane, tos);
+      }
+    }
+    if (mode_reduce(MODE)) {
       s = warp_sum_d(s);
-      combine_partial(p, tp, c, s, lane);
+      combine_partial(p, tp, g, ti.valid ? s : kNaN64, lane);
     }
     u = u_next;
   }

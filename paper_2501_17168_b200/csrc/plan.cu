@@ -48,6 +48,8 @@ constexpr int kReorderMaxLen = kMaxLenSupported;
 constexpr int kDeepPerWarpLevels = 32;
 // k_prepare's row-length tier (two-tier compile when max_len > 2 * kPrepCap)
 constexpr int kPrepCap = 192;
+// kernel (a): most chunks per work unit the plan picks by itself
+constexpr int kMaxUnitChunks = 4;
 
 // instantiated kernels (eval_*.cu): single-output modes at every K the plan
 // uses, multi-output (Modi) modes at K <= 4 (the plan never gives them K = 8)
@@ -222,9 +224,21 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   if (!fn) return EVOGP_E_ARG;
   const int occ = occupancy(fn, 32 * warps, smem, device);
   const int64_t resident = static_cast<int64_t>(sms) * occ;
-  int64_t grid, nseg = 1, seg_chunks = nch;
+  int64_t grid, nseg = 1, seg_chunks = nch, ucs = 1, ngrp = nch;
   if (strategy == EVOGP_STRATEGY_INTER) {
-    const int64_t units = P * nch;
+    // chunks per unit: a unit stages its row and reduces its SSE once, so
+    // more chunks per unit cut that overhead (c2: 17% of the instructions are
+    // outside the interpreter loop) as long as >= 16 units per resident warp
+    // keep the tail short (measured: c3 1 / 2 / 4 chunks 5.99 / 6.17 / 6.27e12;
+    // c2, 8 units per warp at one chunk, loses 2.5% at two)
+    const int64_t rwarps = resident * warps;
+    if (tu.unit_chunks > 0) {
+      ucs = std::min<int64_t>(tu.unit_chunks, std::max<int64_t>(nch, 1));
+    } else {
+      while (ucs < kMaxUnitChunks && nch >= 2 * ucs && P * ((nch + 2 * ucs - 1) / (2 * ucs)) >= 16 * rwarps) ucs *= 2;
+    }
+    ngrp = (nch + ucs - 1) / ucs;
+    const int64_t units = P * ngrp;
     grid = std::max<int64_t>(1, std::min<int64_t>((units + warps - 1) / warps, resident));
   } else {
     // split each tree's datapoints into segments: >= ~8 items per resident CTA
@@ -254,7 +268,9 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   kp.nch = static_cast<int32_t>(nch);
   kp.nseg = static_cast<int32_t>(nseg);
   kp.seg_chunks = static_cast<int32_t>(seg_chunks);
-  kp.nparts = static_cast<int32_t>(strategy == EVOGP_STRATEGY_INTER ? nch : nseg);
+  kp.ucs = static_cast<int32_t>(ucs);
+  kp.ngrp = static_cast<int32_t>(ngrp);
+  kp.nparts = static_cast<int32_t>(strategy == EVOGP_STRATEGY_INTER ? ngrp : nseg);
   kp.SD = SD;
   kp.tree_bytes = tree_bytes;
   kp.warp_smem_bytes = warp_smem;
