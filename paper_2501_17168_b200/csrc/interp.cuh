@@ -187,7 +187,7 @@ __device__ __forceinline__ void vld_nc(const float* p, float (&v)[K]) {
 // COLD = true: same fast paths where valid, library functions elsewhere.
 // ------------------------------------------------------------------------
 // protected log (reading R3): |a| > delta ? log|a| : 0
-__device__ __forceinline__ float fn_plog(float a) { return fabsf(a) > kDelta ? logf(fabsf(a)) : 0.0f; }
+__device__ __forceinline__ float fn_plog(float a) { return fabsf(a) > kDelta ? fm_log(fabsf(a)) : 0.0f; }
 
 // element forms shared by the packed interpreter (hot.cuh): the same
 // expressions as interpret's cases (reading R3)

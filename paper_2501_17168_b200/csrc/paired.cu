@@ -54,7 +54,7 @@ __device__ __forceinline__ float apply_fn(int f, float a, float b, float c) {
     case F_MAX: return fmaxf(a, b);
     case F_MIN: return fminf(a, b);
     case F_POW: return powf(fabsf(a), b);
-    case F_LOG: return fabsf(a) > kDelta ? logf(fabsf(a)) : 0.0f;
+    case F_LOG: return fabsf(a) > kDelta ? fm_log(fabsf(a)) : 0.0f;
     case F_EXP: return expf(a);
     case F_TANH: return tanhf(a);
     case F_NEG: return -a;
