@@ -246,12 +246,16 @@ __device__ __forceinline__ bool interp_multi(const Node* __restrict__ tree, int 
     _Pragma("unroll") for (int k = 0; k < K - 1; ++k) a[k] = a[k + 1]; \
     a[K - 1] = v;                                                 \
   }
-      if (c == HC_LOG) {
-        EVOGP_ROT(fn_plog)
-      } else if (c == HC_EXP) {
+      if (c == HC_EXP) {
         EVOGP_ROT(expf)
-      } else {
+      } else if (c == HC_TANH) {
         EVOGP_ROT(tanhf)
+      } else if (c == HC_SIN) {  // trig with a point beyond 2^40 (the loop's table-free range)
+        EVOGP_ROT(fm_sin_ext)
+      } else if (c == HC_COS) {
+        EVOGP_ROT(fm_cos_ext)
+      } else {
+        EVOGP_ROT(fm_tan_ext)
       }
 #undef EVOGP_ROT
     }
@@ -396,7 +400,7 @@ __device__ __forceinline__ bool interp_hot(const Node* __restrict__ tree, int le
     if (__all_sync(FULL_MASK, m <= kSinCosSmall)) {                                     \
       FOR2 t[j] = pk(APPROX(lo(t[j])), APPROX(hi(t[j])));                               \
     } else if (__any_sync(FULL_MASK, !(m <= kTrigReduceMax))) { /* rare: wide forms */ \
-      bail |= !(m <= kTrigWideMax) && !(absmax_noinf<N2>(t) <= kTrigWideMax);           \
+      bail |= !(m <= kFltMax) && !(absmax_noinf<N2>(t) <= kFltMax);           \
       FOR2 t[j] = pk(EXT(lo(t[j])), EXT(hi(t[j])));                                     \
     } else {                                                                            \
       FOR2 {                                                                            \
@@ -411,7 +415,7 @@ __device__ __forceinline__ bool interp_hot(const Node* __restrict__ tree, int le
     if (__all_sync(FULL_MASK, m <= kTanSmall)) {                                        \
       FOR2 t[j] = poly_tan2(t[j]);                                                      \
     } else if (__any_sync(FULL_MASK, !(m <= kTrigReduceMax))) { /* rare: wide forms */ \
-      bail |= !(m <= kTrigWideMax) && !(absmax_noinf<N2>(t) <= kTrigWideMax);           \
+      bail |= !(m <= kFltMax) && !(absmax_noinf<N2>(t) <= kFltMax);           \
       FOR2 t[j] = pk(fm_tan_ext(lo(t[j])), fm_tan_ext(hi(t[j])));                       \
     } else {                                                                            \
       FOR2 t[j] = tan_full2(t[j]);                                                      \

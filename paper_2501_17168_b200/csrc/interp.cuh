@@ -213,9 +213,9 @@ __device__ __forceinline__ float hot_inv(float a) {
 static __device__ __noinline__ float fold_unary(int f, float c) {
   const float a = fabsf(c);
   switch (f) {
-    case F_SIN: return a <= kTrigWideMax ? fm_sin_ext(c) : slow_sinf(c);
-    case F_COS: return a <= kTrigWideMax ? fm_cos_ext(c) : slow_cosf(c);
-    case F_TAN: return a <= kTrigWideMax ? fm_tan_ext(c) : slow_tanf(c);
+    case F_SIN: return a <= kFltMax ? fm_sin_ext(c) : slow_sinf(c);
+    case F_COS: return a <= kFltMax ? fm_cos_ext(c) : slow_cosf(c);
+    case F_TAN: return a <= kFltMax ? fm_tan_ext(c) : slow_tanf(c);
     case F_LOG: return fn_plog(c);
     case F_EXP: return expf(c);
     case F_TANH: return tanhf(c);
@@ -417,9 +417,9 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
   }
       DIV_CASE(OP_FN + F_DIV, tos, b)
       DIV_CASE(OP_FN + F_DIV_R, b, tos)  // children swapped by the compile pass
-      UN_RANGED(F_SIN, kTrigWideMax, fm_sin_ext, slow_sinf(a), kSinCosSmall, fm_sin_small)
-      UN_RANGED(F_COS, kTrigWideMax, fm_cos_ext, slow_cosf(a), kSinCosSmall, fm_cos_small)
-      UN_RANGED(F_TAN, kTrigWideMax, fm_tan_ext, slow_tanf(a), kTanSmall, fm_tan_small)
+      UN_RANGED(F_SIN, kFltMax, fm_sin_ext, slow_sinf(a), kSinCosSmall, fm_sin_small)
+      UN_RANGED(F_COS, kFltMax, fm_cos_ext, slow_cosf(a), kSinCosSmall, fm_cos_small)
+      UN_RANGED(F_TAN, kFltMax, fm_tan_ext, slow_tanf(a), kTanSmall, fm_tan_small)
       BIN(F_MAX, fmaxf(a, bb))
       BIN(F_MIN, fminf(a, bb))
 // pow(|BASE|, EXPO): one inlined powf body applied to the K points by
@@ -554,9 +554,9 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
         BIN(F_MUL, __fmul_rn(a, bb))
         DIV_CASE(OP_FN + F_DIV, tos, b)
         DIV_CASE(OP_FN + F_DIV_R, b, tos)
-        UN_RANGED(F_SIN, kTrigWideMax, fm_sin_ext, slow_sinf(a), kSinCosSmall, fm_sin_small)
-        UN_RANGED(F_COS, kTrigWideMax, fm_cos_ext, slow_cosf(a), kSinCosSmall, fm_cos_small)
-        UN_RANGED(F_TAN, kTrigWideMax, fm_tan_ext, slow_tanf(a), kTanSmall, fm_tan_small)
+        UN_RANGED(F_SIN, kFltMax, fm_sin_ext, slow_sinf(a), kSinCosSmall, fm_sin_small)
+        UN_RANGED(F_COS, kFltMax, fm_cos_ext, slow_cosf(a), kSinCosSmall, fm_cos_small)
+        UN_RANGED(F_TAN, kFltMax, fm_tan_ext, slow_tanf(a), kTanSmall, fm_tan_small)
         BIN(F_SUB_R, __fsub_rn(bb, a))
         default:
           bail = true;

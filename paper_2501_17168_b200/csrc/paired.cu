@@ -48,9 +48,9 @@ __device__ __forceinline__ float apply_fn(int f, float a, float b, float c) {
       const bool fast = fabsf(a) <= kDivRange && fabsf(b) <= kDivRange && (a == 0.0f || fabsf(a) >= kDivRangeMin);
       return fabsf(b) > kDelta ? (fast ? div_fast(a, b) : slow_div(a, b)) : 1.0f;
     }
-    case F_SIN: return fabsf(a) <= kTrigWideMax ? fm_sin_ext(a) : slow_sinf(a);
-    case F_COS: return fabsf(a) <= kTrigWideMax ? fm_cos_ext(a) : slow_cosf(a);
-    case F_TAN: return fabsf(a) <= kTrigWideMax ? fm_tan_ext(a) : slow_tanf(a);
+    case F_SIN: return fabsf(a) <= kFltMax ? fm_sin_ext(a) : slow_sinf(a);
+    case F_COS: return fabsf(a) <= kFltMax ? fm_cos_ext(a) : slow_cosf(a);
+    case F_TAN: return fabsf(a) <= kFltMax ? fm_tan_ext(a) : slow_tanf(a);
     case F_MAX: return fmaxf(a, b);
     case F_MIN: return fminf(a, b);
     case F_POW: return powf(fabsf(a), b);

@@ -556,10 +556,13 @@ def test_fast_trig_accuracy():
     kk = np.exp2(rng.uniform(16, 30, 1 << 16)).astype(np.int64)
     near_w = (kk * (np.pi / 2)).astype(np.float32).astype(np.float64)
     near_w = np.concatenate([near_w, np.nextafter(near_w.astype(np.float32), np.float32(np.inf)).astype(np.float64)])
+    # the table tier (|x| > 2^40 to FLT_MAX): log-uniform over the whole exponent range
+    huge = np.sign(rng.standard_normal(1 << 18)) * np.exp2(rng.uniform(40, 127.99, 1 << 18))
     xs = np.concatenate([rng.uniform(-10, 10, 1 << 20), rng.uniform(-1e5, 1e5, 1 << 19),
                          np.sign(rng.standard_normal(1 << 18)) * 10 ** rng.uniform(-8, 0, 1 << 18), near,
-                         rng.uniform(1e5, 1e7, 4096), wide, near_w,
-                         np.array([0.0, -0.0, 1e30, -1e30, 105615.0, 105616.0, 2.0 ** 40, -(2.0 ** 40), 1.2e12])
+                         rng.uniform(1e5, 1e7, 4096), wide, near_w, huge,
+                         np.array([0.0, -0.0, 1e30, -1e30, 105615.0, 105616.0, 2.0 ** 40, -(2.0 ** 40), 1.2e12,
+                                   3.4028235e38, -3.4028235e38, 2.0 ** 104, 1.0995118e12])
                          ]).astype(np.float32)
     pt = synth.PrefixTrees(np.array([0, 2, 4, 6], np.int64), np.array([2, 1, 2, 1, 2, 1], np.int16),
                            np.array([4, 0, 5, 0, 6, 0], np.float32))
@@ -582,27 +585,40 @@ TRIG_ABS = 2.0 ** -20  # absolute error budget of sin.approx / cos.approx on [-p
 
 def test_trig_wide_hot_equals_cold():
     """A point's sin / cos / tan value does not depend on which interpreter
-    copy ran: the same arguments (105615 < |x| <= 2^40, the wide forms, and
-    the FP32 range) once in chunks that stay hot and once in chunks that
-    re-run cold (one x1 = 1e30 per chunk sends the chunk to the library
-    copy, whose result is multiplied by zero)."""
+    copy ran. The same arguments (the FP32 range; 105615 < |x| <= 2^40, the
+    FP64 forms; 2^40 < |x| <= FLT_MAX, the table forms) are evaluated once in
+    chunks that stay hot and once in chunks that re-run cold (one x1 = 1e30
+    per 32 points puts a division beyond its fast range, 0 * (x1 / x1), into
+    every chunk), through the paper-set loop, the full-set packed loop (a MAX
+    node makes the row full-set) and the multi-output loop (a Modi root)."""
     rng = np.random.default_rng(12)
     n = 1 << 16
     x0 = np.concatenate([np.sign(rng.standard_normal(n)) * np.exp2(rng.uniform(0, 40, n)),
+                         np.sign(rng.standard_normal(n)) * np.exp2(rng.uniform(40, 127.99, n)),
                          rng.uniform(-4, 4, 1024)]).astype(np.float32)
-    # f(x0) + 0 * sin(x1): ADD, f, x0, MUL, 0, SIN, x1   (f = sin, cos, tan)
-    pt = synth.PrefixTrees(np.array([0, 7, 14, 21], np.int64),
-                           np.array([3, 2, 1, 3, 0, 2, 1] * 3, np.int16),
-                           np.array([v for f in (4, 5, 6) for v in (0, f, 0, 2, 0, 4, 1)], np.float32))
-    dt = to_device(pt, 7, 2)
     hot = np.stack([x0, np.ones_like(x0)], axis=1)
     cold = hot.copy()
-    cold[::32, 1] = 1e30  # one per 32 points: every chunk of every kernel re-runs cold
-    for strategy in ("inter", "intra"):
-        gh = gpu_eval(dt, hot, 1, strategy)[:, :, 0]
-        gc = gpu_eval(dt, cold, 1, strategy)[:, :, 0]
-        ok = (gh == gc) | (np.isnan(gh) & np.isnan(gc))
-        assert ok.all(), (strategy, (~ok).sum(), x0[np.nonzero(~ok)[1][:4]])
+    cold[::32, 1] = 1e30
+    for variant in ("paper", "full", "modi"):
+        # ADD(f(a), MUL(0, DIV(x1, x1))), a = x0 (paper) or MAX(x0, x0)
+        tys, vas = [], []
+        for f in (4, 5, 6):
+            root = 3 | (8 if variant == "modi" else 0)  # Modi root, slot 0
+            if variant == "paper":
+                tys += [root, 2, 1, 3, 0, 3, 1, 1]
+                vas += [0, f, 0, 2, 0, 3, 1, 1]
+            else:
+                tys += [root, 2, 3, 1, 1, 3, 0, 3, 1, 1]
+                vas += [0, f, 7, 0, 0, 2, 0, 3, 1, 1]
+        ln = 8 if variant == "paper" else 10
+        pt = synth.PrefixTrees(np.arange(4, dtype=np.int64) * ln, np.array(tys, np.int16), np.array(vas, np.float32))
+        n_out = 2 if variant == "modi" else 1
+        dt = to_device(pt, ln, 2, n_out)
+        for strategy in ("inter", "intra"):
+            gh = gpu_eval(dt, hot, n_out, strategy)[:, :, 0]
+            gc = gpu_eval(dt, cold, n_out, strategy)[:, :, 0]
+            ok = (gh == gc) | (np.isnan(gh) & np.isnan(gc))
+            assert ok.all(), (variant, strategy, (~ok).sum(), x0[np.nonzero(~ok)[1][:4]])
 
 
 def test_ieee_fast_paths_bitexact():
