@@ -389,6 +389,44 @@ def test_edge_malformed_row_nan_and_flag():
         assert evogp.check_device_flags(ws) == 0
 
 
+def test_two_tier_compile_malformed_and_boundary_rows():
+    """max_len 512 takes the two-tier compile pass (rows of up to 192 nodes in
+    k_prepare, longer ones queued for k_prepare_long): rows of 192 / 193 /
+    512 nodes and malformed rows in both tiers (a length beyond max_len, a
+    zero length, a leftover operand in a long row) give the oracle's values
+    or NaN + the device flag."""
+    evogp = _evogp()
+    L, n_in, D = 512, 2, 300
+    offs, tys, vas = [0], [], []
+    for n in (1, 63, 191, 192, 193, 256, 401, 511, 192, 401):  # left combs of ADD (even n: under a NEG)
+        if n % 2 == 0:
+            tys.append(2)
+            vas.append(13.0)
+        nf = (n - 1 - (n % 2 == 0)) // 2  # the comb has n (odd n) or n - 1 nodes
+        tys += [3] * nf + [1] * (nf + 1)
+        vas += [0.0] * nf + [float(k % n_in) for k in range(nf + 1)]
+        offs.append(len(tys))
+    pt = synth.PrefixTrees(np.array(offs, np.int64), np.array(tys, np.int16), np.array(vas, np.float32))
+    t, v, s = evogp.tensorize(pt.offsets, pt.types, pt.values, L, n_in)
+    t, v, s = t.copy(), v.copy(), s.copy()
+    s[8, 0] = 0          # zero length (small tier)
+    s[9, 0] = L + 7      # beyond max_len (queued for the long tier)
+    t[7, 0] = 1          # a 511-node row whose root is a VAR: leftover operands (long tier)
+    v[7, 0] = 0
+    bad = [7, 8, 9]
+    X = synth.dataset_X(13, 0, D, n_in, lo=0.5, hi=1.5)
+    r32 = oracle.evaluate(*oracle_arrays(pt, L, n_in), X, mode=1)[:, :, 0]
+    dev = [torch.from_numpy(a).cuda() for a in (t, v, s)]
+    Xd = torch.from_numpy(X).cuda()
+    for strategy in ("inter", "intra"):
+        ws = evogp.Workspace(10, D, L, n_in, 1, device="cuda:0")
+        g = evogp.eval(*dev, Xd, strategy=strategy, workspace=ws).cpu().numpy()[:, :, 0]
+        assert evogp.check_device_flags(ws) & 1, strategy
+        good = [i for i in range(10) if i not in bad]
+        assert same_bits_mod_zero(g[good], r32[good]).all(), strategy
+        assert np.isnan(g[bad]).all(), strategy
+
+
 def test_data_shard_algebra_single_gpu():
     """sum over row-shards of evogp_sr_sse == full SSE (FP64 re-association
     only), i.e. the datapoint-sharded multi-GPU algebra, on one GPU."""
