@@ -131,7 +131,7 @@ struct alignas(8) TreeMeta {
 struct Control {
   int32_t flags;            // device flags (bit 0: malformed row evaluated as NaN)
   uint32_t cold_chunks;     // chunks re-run on the cold interpreter copy (diagnostic, per call)
-  unsigned long long work;  // dynamic work-queue ticket counter (zeroed by k_stage_x)
+  unsigned long long work;  // dynamic work-queue ticket counter (zeroed by k_prepare)
   unsigned long long deep;  // deep-stack pool ticket counter
   uint32_t nlong;           // rows queued for k_prepare_long (zeroed before k_prepare when it runs)
   uint32_t pad_;
