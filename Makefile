@@ -7,7 +7,7 @@ LIB := $(PKG)/libevogp.so
 NVFLAGS := -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
            -ftz=false -prec-div=true -prec-sqrt=true -Xcompiler -fPIC,-O2 -Xptxas -v
 # one translation unit per evaluation-kernel family so `make -j` builds them in parallel
-CU := eval_inter_k16 eval_intra_k16 eval_inter_k8 eval_inter_k4 eval_inter_k2 eval_inter_k1 eval_intra_k8 eval_intra_k4 compile plan \
+CU := eval_full eval_inter_k16 eval_intra_k16 eval_inter_k8 eval_inter_k4 eval_inter_k2 eval_inter_k1 eval_intra_k8 eval_intra_k4 compile plan \
       paired variation tensorize_dev capi
 OBJDIR := build/obj
 OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU))) $(OBJDIR)/tensorize.o

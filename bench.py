@@ -82,7 +82,7 @@ def measured_peaks():
 
 
 def default_mix(cfg):
-    return "full" if cfg.n_out > 1 else "paper"
+    return "full" if (cfg.n_out > 1 or cfg.eval_only) else "paper"
 
 
 def workload_desc(cfg, mix):
@@ -191,7 +191,7 @@ def oracle_pass(pt, cfg, X, y, threads):
         oracle.evaluate_paired(t, v, s, X.reshape(t.shape[0], cfg.D, cfg.n_in), n_out=cfg.n_out, mode=0)
         return
     out = oracle.evaluate(t, v, s, X, n_out=cfg.n_out, mode=0, threads=threads)
-    if cfg.n_out == 1:
+    if cfg.n_out == 1 and not cfg.eval_only:
         oracle.mse(out[:, :, 0], y)
 
 
@@ -541,7 +541,8 @@ def main():
         chosen = (evogp.select_strategy(P_local, D_local, cfg.max_len, cfg.n_out, local) if strategy == "auto"
                   else strategy)
     ws = evogp.Workspace(P_local, D_local, cfg.max_len, cfg.n_in, cfg.n_out, device=dev)
-    out_eval = torch.empty((P_local, D_local, cfg.n_out), dtype=torch.float32, device=dev) if cfg.n_out > 1 else None
+    evalcfg = cfg.n_out > 1 or cfg.eval_only  # outputs only (evogp_eval), no fitness
+    out_eval = torch.empty((P_local, D_local, cfg.n_out), dtype=torch.float32, device=dev) if evalcfg else None
     if cfg.paired:
         out_eval = torch.empty(((P_local, cfg.n_out) if cfg.D == 1 else (P_local, cfg.D, cfg.n_out)),
                                dtype=torch.float32, device=dev)
@@ -555,7 +556,7 @@ def main():
         if cfg.paired:
             evogp.eval_paired(td, vd, sd, Xd, n_outputs=cfg.n_out, out=out_eval, workspace=ws)
             return out_eval
-        if cfg.n_out > 1:
+        if evalcfg:
             evogp.eval(td, vd, sd, Xd, n_outputs=cfg.n_out, strategy=strategy, out=out_eval, workspace=ws)
             return out_eval
         if axis == "data":
@@ -619,6 +620,11 @@ def main():
         dist.all_reduce(work, op=dist.ReduceOp.SUM)
     step_ms, kern_ms = tt.tolist()
     total_work = work.item()  # node x datapoint evaluations per step, all ranks
+    # config 5: the fraction of (tree, output slot) pairs some
+    # Modi node wrote (slots no Modi node targets stay 0, reading R4)
+    modi_nonzero = None
+    if cfg.n_out > 1 and out_eval is not None:
+        modi_nonzero = float((out_eval != 0).flatten(0, -3).any(dim=-2).float().mean().item()) if out_eval.dim() == 3 else None
     value = total_work * args.steps / (step_ms * 1e-3)
 
     # ---- launch-bound configs (c1): the same step replayed from a CUDA graph
@@ -661,8 +667,8 @@ def main():
         h_off, h_ty, h_va = pin(pt.offsets.astype(np.int64)), pin(pt.types), pin(pt.values)
         d_off, d_ty, d_va = (torch.empty_like(x, device=dev) for x in (h_off, h_ty, h_va))
         h_X, h_y = pin(X), pin(y)
-        res_len = P_total if (cfg.n_out == 1) else P_local * D_local * cfg.n_out
-        h_res = torch.empty(res_len, dtype=torch.float64 if cfg.n_out == 1 else torch.float32).pin_memory()
+        res_len = P_total if not evalcfg else P_local * D_local * cfg.n_out
+        h_res = torch.empty(res_len, dtype=torch.float32 if evalcfg else torch.float64).pin_memory()
         h2d = sum(x.numel() * x.element_size() for x in (h_off, h_ty, h_va, h_X, h_y))
         d2h = h_res.numel() * h_res.element_size()
 
@@ -678,7 +684,7 @@ def main():
         e2e_mode = "one pass"
         n_chunks = int(os.environ.get("EVOGP_E2E_CHUNKS", "1"))  # with 2 steps in flight, chunking measured no gain (c4) or a loss (c2)
         depth = min(2, int(os.environ.get("EVOGP_E2E_DEPTH", "2")))  # two host result buffers
-        if cfg.n_out == 1 and not use_dist and not cfg.paired and (n_chunks > 1 or depth > 1):
+        if not evalcfg and not use_dist and not cfg.paired and (n_chunks > 1 or depth > 1):
             # single-output populations: the streaming public path. Copies of
             # chunk c+1 overlap the device work of chunk c; with depth 2 the
             # next step's copies (its trees AND its dataset) also overlap this
@@ -739,7 +745,7 @@ def main():
                 pj = json.load(fh)
             traffic, traffic_src = pj.get("dram_bytes_per_launch"), f"profiles/{os.path.basename(prof)} ({pj.get('note', '')})"
         hbm_view = None
-        if cfg.n_out > 1 and not cfg.paired:
+        if evalcfg and not cfg.paired:
             # multi-output eval: the P x D x n_out FP32 output store is the one
             # HBM-relevant stream: report it against HBM
             out_bytes = 4.0 * P_local * D_local * cfg.n_out
@@ -762,10 +768,11 @@ def main():
                        "strategy": chosen,
                        "parallelism": f"{axis}-shard x{world}" + (" (NCCL)" if use_dist else " (no collective)"),
                        "cold_rerun_chunks_last_step": cold_chunks,
+                       **({"modi_nonzero_slot_fraction": modi_nonzero} if modi_nonzero is not None else {}),
                        "l2": "flushed (256 MiB write) before every timed step",
                        "step": ("evogp_eval_paired" if cfg.paired else
-                                "evogp_eval" if cfg.n_out > 1 else "evogp_sr_fitness") +
-                               (" + NCCL combine" if use_dist and cfg.n_out == 1 and not cfg.paired else "")},
+                                "evogp_eval" if evalcfg else "evogp_sr_fitness") +
+                               (" + NCCL combine" if use_dist and not evalcfg and not cfg.paired else "")},
             "roofline": ({"bound": "alu", "achieved": achieved, "peak": roof, "unit": UNIT, "frac": achieved / roof,
                           "traffic": traffic, "traffic_source": traffic_src, "kernel": f"k_{chosen}",
                           "peak_basis": f"{SMS} SMs x min({FP32_LANES} FP32, {SFU_LANES}/s MUFU) lanes/clk at "

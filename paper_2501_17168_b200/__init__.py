@@ -317,11 +317,11 @@ def check_device_flags(workspace: Workspace, stream=None) -> int:
 
 
 def set_tuning(target_warps: int = 0, no_reorder: bool = False, no_fuse: bool = False, K: int = 0,
-               reorder_above: int = 0, unit_chunks: int = 0) -> None:
+               reorder_above: int = 0, unit_chunks: int = 0, full_set: bool = False) -> None:
     """evogp_set_tuning for this thread (calibration sweeps, tests); all
     defaults = the library's own plan. Results never depend on it."""
     t = _lib.Tuning(int(target_warps), int(bool(no_reorder)), int(bool(no_fuse)), int(K), int(reorder_above),
-                    int(unit_chunks))
+                    int(unit_chunks), int(bool(full_set)))
     st = _LIB.evogp_set_tuning(ctypes.byref(t))
     if st != OK:
         raise EvogpError(st, "evogp_set_tuning")

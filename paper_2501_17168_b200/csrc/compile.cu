@@ -132,7 +132,7 @@ __device__ int reorder_program(const Node* s_nodes, int n, Node* row, unsigned c
 // Returns the new length (and *depth_out), or -1 when the sizes are
 // inconsistent. Scratch after the decoded nodes: 12 L bytes.
 __device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __restrict__ urow_size, Node* row,
-                                unsigned char* scr, int L, int lane, int* depth_out, bool reorder) {
+                                unsigned char* scr, int L, int lane, int* depth_out, bool reorder, bool fuse = true) {
   uint16_t* sz = reinterpret_cast<uint16_t*>(scr);
   uint16_t* nd = sz + L;  // the absorbed-prefix counts by new position
   int32_t* diff = reinterpret_cast<int32_t*>(nd + L);  // 4L bytes in: 4-byte aligned
@@ -217,7 +217,7 @@ __device__ int reorder_fuse_par(const Node* s_nodes, int n, const int16_t* __res
   // whose first-visited child is not a leaf absorbs its second-visited child
   // when that is a leaf (operand b is then the leaf, under the unreversed
   // op: g(F1, leaf)). The last node is never absorbed (it starts the stack).
-  for (int j = lane; j < n; j += 32) {
+  for (int j = lane; j < n && fuse; j += 32) {
     const int ar = ar_of(s_nodes[j + 1].w0);
     if (ar == 0 || ar > 2) continue;
     const int c1 = j + 1;
@@ -342,9 +342,11 @@ __device__ void compile_row_warp(const KParams& p, int64_t tp, unsigned char* sc
       // that need no reordering also take fuse_copy: the second-child fusion
       // of reorder_fuse_par(reorder = false) measured +1-2% in the kernels
       // but -5% on c4's whole step (the compile pass costs more than it saves)
+      // (fusion for paper-set rows only: the other single-output rows run
+      // the full-set PTX loop, which has no fused-operand forms)
       int dep = ti.maxdepth;
       const int len = reorder_fuse_par(s_nodes, ti.len, p.size + tp * p.ld, row, scratch + (Lc + 1) * 8, Lc,
-                                       lane, &dep, true);
+                                       lane, &dep, true, ti.paper);
       if (len > 0) {
         ti.len = len;
         ti.maxdepth = dep;
@@ -356,7 +358,7 @@ __device__ void compile_row_warp(const KParams& p, int64_t tp, unsigned char* sc
         prog = s_reord;
       }
     }
-    if (ti.valid && p.fuse) {
+    if (ti.valid && p.fuse && ti.paper) {
       ti.len = fuse_copy(prog, ti.len, row, lane);
     } else {
       for (int i = lane; i <= ti.len; i += 32) {

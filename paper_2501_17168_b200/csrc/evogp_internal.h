@@ -227,6 +227,8 @@ const void* kernel_inter_k16(int mode);
 const void* kernel_intra_k4(int mode);
 const void* kernel_intra_k8(int mode);
 const void* kernel_intra_k16(int mode);
+// eval_full.cu: the full-set variants (single-output modes, K = 4 / 8)
+const void* kernel_full(int strategy, int K, int mode);
 
 // paired.cu
 int launch_paired(const int16_t* type, const float* value, const int16_t* size, int64_t P, int32_t L, int32_t ld,

@@ -217,7 +217,8 @@ __device__ __forceinline__ bool interp_multi(const Node* __restrict__ tree, int 
     float a[K], rt[K];
 #pragma unroll
     for (int j = 0; j < N2; ++j) unpk(t[j], a[2 * j], a[2 * j + 1]);
-    if (c == HC_POW) {  // pow(|a|, b), b popped (the rightmost child)
+    if (c == HC_POW || c == HC_POWR) {  // pow(|a|, b), b popped (the rightmost child); POW_R: pow(|b|, a)
+      const bool rev = c == HC_POWR;
       top -= SLOT * 4;
       vld<K>(stk + (top - top0) / 4, rt);
       float e[K];
@@ -225,7 +226,7 @@ __device__ __forceinline__ bool interp_multi(const Node* __restrict__ tree, int 
       for (int k = 0; k < K; ++k) e[k] = rt[k];
 #pragma unroll 1
       for (int it = 0; it < K; ++it) {  // one inlined powf body, register rotation
-        const float v = powf(fabsf(a[0]), e[0]);
+        const float v = powf(fabsf(rev ? e[0] : a[0]), rev ? a[0] : e[0]);
         const float e0 = e[0];
 #pragma unroll
         for (int k = 0; k < K - 1; ++k) {

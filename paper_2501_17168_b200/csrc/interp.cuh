@@ -675,7 +675,7 @@ __device__ __forceinline__ void run_passes(const Node* tree, int len, const floa
 // a fast path's range is re-run on the cold copy. Rows deeper than every
 // pass split use a global stack: the warp's private slot (no contention) when
 // it is deep enough, else a slot of the locked pool.
-template <int K, bool MULTI>
+template <int K, bool MULTI, bool FULL = false>
 __device__ __forceinline__ void run_chunk(const KParams& p, const Node* tree, const TreeInfo& ti, int64_t chunk_base,
                                           int lane, float* s_stack_l, float* s_acc_l, float (&tos)[K]) {
   constexpr int V = Lay<K>::V;
@@ -684,8 +684,17 @@ __device__ __forceinline__ void run_chunk(const KParams& p, const Node* tree, co
   const int need = ti.maxdepth - 1;  // stack slots below the register top
   if (need <= p.SD) {
     bool bail;
-    if constexpr (!MULTI && K >= 4) {
-      // single-output programs carry hot codes (compile pass): packed interpreter
+    if constexpr (!MULTI && FULL && (K == 4 || K == 8)) {
+      // single-output programs carry hot codes (compile pass): the paper-set
+      // PTX loop for paper-set rows (fused operands); in the full-set kernel
+      // variants the others run the full-set PTX loop of the multi-output
+      // rows (unfused, no Modi node: the result is the top of the stack). The
+      // default variants keep that loop's code out of the kernel (it cost the
+      // paper-set loop 2-15% by its size and register pressure) and run the
+      // C++ full-set loop instead.
+      bail = ti.paper ? hot::interp_hot<K, true>(tree, ti.len, xl, s_stack_l, tos)
+                      : hot::interp_multi<K>(tree, ti.len, xl, s_stack_l, s_acc_l, tos);
+    } else if constexpr (!MULTI && K >= 4) {
       bail = ti.paper ? hot::interp_hot<K, true>(tree, ti.len, xl, s_stack_l, tos)
                       : hot::interp_hot<K, false>(tree, ti.len, xl, s_stack_l, tos);
     } else if constexpr (MULTI && (K == 4 || K == 8)) {
@@ -919,7 +928,7 @@ __device__ __forceinline__ long long next_ticket(const KParams& p, int lane) {
   return static_cast<long long>(__shfl_sync(FULL_MASK, t, 0));
 }
 
-template <int K, int MODE>
+template <int K, int MODE, bool FULL = false>
 __global__ void __launch_bounds__(32 * kInterWarps, (K >= 16 || (K == 8 && mode_multi(MODE))) ? 4 : 8)
     k_inter(const KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -958,7 +967,7 @@ __global__ void __launch_bounds__(32 * kInterWarps, (K >= 16 || (K == 8 && mode_
       const int64_t chunk_base = static_cast<int64_t>(c) * (32 * K);
       float tos[K];
       if (mode_multi(MODE) && !ti.valid) zero_acc<K>(s_acc_l, p.n_out);
-      if (ti.valid) run_chunk<K, mode_multi(MODE)>(p, s_tree, ti, chunk_base, lane, s_stack_l, s_acc_l, tos);
+      if (ti.valid) run_chunk<K, mode_multi(MODE), FULL>(p, s_tree, ti, chunk_base, lane, s_stack_l, s_acc_l, tos);
       if (MODE == MODE_EVAL1) {
         store_out1<K>(p, tp, chunk_base, lane, tos, ti.valid);
       } else if (MODE == MODE_EVALN) {
@@ -981,7 +990,7 @@ __global__ void __launch_bounds__(32 * kInterWarps, (K >= 16 || (K == 8 && mode_
 // ------------------------------------------------------------------------
 
 
-template <int K, int MODE>
+template <int K, int MODE, bool FULL = false>
 __global__ void __launch_bounds__(32 * kIntraWarps, (K >= 16 || (K == 8 && mode_multi(MODE))) ? 2 : 4)
     k_intra(const KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1048,7 +1057,7 @@ __global__ void __launch_bounds__(32 * kIntraWarps, (K >= 16 || (K == 8 && mode_
       const int64_t chunk_base = static_cast<int64_t>(c) * (32 * K);
       float tos[K];
       if (mode_multi(MODE) && !ti.valid) zero_acc<K>(s_acc_l, p.n_out);
-      if (ti.valid) run_chunk<K, mode_multi(MODE)>(p, s_tree, ti, chunk_base, lane, s_stack_l, s_acc_l, tos);
+      if (ti.valid) run_chunk<K, mode_multi(MODE), FULL>(p, s_tree, ti, chunk_base, lane, s_stack_l, s_acc_l, tos);
       if (MODE == MODE_EVAL1) {
         store_out1<K>(p, tp, chunk_base, lane, tos, ti.valid);
       } else if (MODE == MODE_EVALN) {

@@ -55,6 +55,7 @@ constexpr int kMaxUnitChunks = 4;
 // uses, multi-output (Modi) modes at K <= 4 (the plan never gives them K = 8)
 const void* kernel_ptr(int strategy, int K, int mode) {
   const bool multi = mode_multi(mode);
+  if (tuning().full_set != 0 && !multi && (K == 4 || K == 8)) return kernel_full(strategy, K, mode);
   if (strategy == EVOGP_STRATEGY_INTER) {
     switch (K) {
       case 1: return kernel_inter_k1(mode);

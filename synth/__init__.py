@@ -130,6 +130,7 @@ class Config:
     index: int
     paired: bool = False  # NEXT-2: D = observations per individual (B), each tree on its own
     loop: bool = False  # NEXT-4: the whole generational loop (Algorithm 1), population generated on device
+    eval_only: bool = False  # outputs only (evogp_eval), no fitness: config 5's alternative reading
 
     @property
     def seed(self) -> int:
@@ -142,6 +143,10 @@ CONFIGS = {
     "c3": Config("c3_intra", 1000, 127, 8, 1, 1 << 20, "uniform", -1.0, 1.0, 0.0, 3),
     "c4": Config("c4_large_pop", 1_000_000, 127, 8, 1, 256, "uniform", -1.0, 1.0, 0.0, 4),
     "c5": Config("c5_multi_output", 10_000, 63, 17, 6, 4096, "normal", 0.0, 0.0, 0.1, 5),
+    # config 5's alternative reading: "10^4 individuals x 6 output
+    # trees" as 6 x 10^4 independent single-output trees, outputs only
+    "c5b": Config("c5b_six_single_output_trees", 60_000, 63, 17, 1, 4096, "normal", 0.0, 0.0, 0.0, 8,
+                  eval_only=True),
     # NEXT-2: one control step of 10^6 policy trees, each on
     # its own 17-dim observation, 6 Modi outputs (shapes from config 5)
     "n2": Config("n2_paired_policy", 1_000_000, 63, 17, 6, 1, "normal", 0.0, 0.0, 0.1, 6, True),

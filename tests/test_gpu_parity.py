@@ -220,6 +220,32 @@ def test_tier_d_kernels_bit_identical(mix, n_out, modi, n_in):
         assert np.allclose(ma[fin], mb[fin], rtol=1e-12, atol=0)
 
 
+@pytest.mark.parametrize("strategy", ["inter", "intra"])
+def test_full_set_variant_bit_identical(strategy):
+    """The full-set kernel variant (tuning full_set: single-output full-set
+    rows on the packed multi loop instead of the scalar C++ interpreter)
+    changes where a node is computed, never its value: outputs bit-identical
+    to the default kernels on the full mix (libm escapes, huge trig, protected
+    division and its fix-ups), IEEE rows bit-exact to the oracle, and the
+    fused MSE identical to the bit."""
+    P, L, n_in, D = 300, 63, 4, 5000
+    pt, X, y = make_case(410, P, L, n_in, D, "full")
+    dt = to_device(pt, L, n_in)
+    a, ma = gpu_eval(dt, X, 1, strategy), gpu_mse(dt, X, y, strategy)
+    with tuning(full_set=True):
+        b, mb = gpu_eval(dt, X, 1, strategy), gpu_mse(dt, X, y, strategy)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert np.array_equal(ma.view(np.uint64), mb.view(np.uint64))
+    pt, X, _ = make_case(411, P, L, 6, 4096, "ieee", dist="normal")
+    dt = to_device(pt, L, 6)
+    with tuning(full_set=True):
+        g = gpu_eval(dt, X, 1, strategy)[:, :, 0]
+    t, v, s = oracle_arrays(pt, L, 6)
+    r32 = oracle.evaluate(t, v, s, X, mode=1)[:, :, 0]
+    ok = same_bits_mod_zero(g, r32)
+    assert ok.all(), (~ok).sum()
+
+
 def test_determinism():
     pt, X, y = make_case(500, 500, 63, 4, 4096, "paper")
     dt = to_device(pt, 63, 4)
