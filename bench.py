@@ -520,8 +520,13 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
 
-    if args.tune:
-        evogp.set_tuning(**{k: int(v) for k, v in (kv.split("=") for kv in args.tune.split(","))})
+    tune = {k: int(v) for k, v in (kv.split("=") for kv in args.tune.split(","))} if args.tune else {}
+    if mix != "paper" and cfg.n_out == 1 and not cfg.paired:
+        # full-set single-output population: the full-set kernel variants
+        # (evogp_tuning.full_set, include/evogp.h), unless --tune says otherwise
+        tune.setdefault("full_set", 1)
+    if tune:
+        evogp.set_tuning(**tune)
     axis, (p0, p1), (d0, d1) = local_shards(cfg, rank, world, args.scaling)
     pt = synth.trees(cfg.seed, p0, p1 - p0, cfg.max_len, synth.MIXES[mix], cfg.n_in, cfg.n_out, cfg.modi_prob)
     if cfg.paired:  # NEXT-2: every individual's own B observations, rows p0*B ...
@@ -765,7 +770,7 @@ def main():
                        "D_per_rank": D_local,
                        "max_len": cfg.max_len, "n_inputs": cfg.n_in, "n_outputs": cfg.n_out,
                        "mean_len": nodes / max(1, P_local), "sfu_node_fraction": sfu_frac,
-                       "strategy": chosen,
+                       "strategy": chosen, **({"tuning": tune} if tune else {}),
                        "parallelism": f"{axis}-shard x{world}" + (" (NCCL)" if use_dist else " (no collective)"),
                        "cold_rerun_chunks_last_step": cold_chunks,
                        **({"modi_nonzero_slot_fraction": modi_nonzero} if modi_nonzero is not None else {}),

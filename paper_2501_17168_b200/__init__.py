@@ -11,7 +11,9 @@ P:221-258): ``type`` int16, ``value`` float32, ``size`` int16, each P x ld.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import threading
 
 import numpy as np
 
@@ -23,7 +25,7 @@ _LIB = _lib.load()
 
 __all__ = [
     "tensorize", "tensorize_device", "eval", "sr_fitness", "sr_sse", "classification_accuracy", "eval_paired", "select_strategy", "workspace_size", "Workspace",
-    "check_device_flags", "EvogpError", "last_launch_count", "set_tuning", "set_kernel_timing", "STRATEGIES",
+    "check_device_flags", "EvogpError", "last_launch_count", "set_tuning", "tuning_hint", "set_kernel_timing", "STRATEGIES",
     "GPConfig", "generate", "subtree_exchange", "tournament", "reproduce", "Evolution",
 ]
 
@@ -325,6 +327,24 @@ def set_tuning(target_warps: int = 0, no_reorder: bool = False, no_fuse: bool = 
     st = _LIB.evogp_set_tuning(ctypes.byref(t))
     if st != OK:
         raise EvogpError(st, "evogp_set_tuning")
+    _TUNING.kw = dict(target_warps=target_warps, no_reorder=no_reorder, no_fuse=no_fuse, K=K,
+                      reorder_above=reorder_above, unit_chunks=unit_chunks, full_set=full_set)
+
+
+_TUNING = threading.local()
+
+
+@contextlib.contextmanager
+def tuning_hint(**kw):
+    """The thread's current tuning with ``kw`` overriding it for the body of a
+    with-block, then restored (e.g. ``full_set=True`` around calls on a
+    population drawn from the full function set)."""
+    prev = dict(getattr(_TUNING, "kw", {}))
+    set_tuning(**{**prev, **kw})
+    try:
+        yield
+    finally:
+        set_tuning(**prev)
 
 
 def last_launch_count() -> int:

@@ -124,7 +124,11 @@ int select_strategy(int64_t P, int64_t D, int32_t L, int32_t n_out, int device) 
   if (sms != 148) return D >= static_cast<int64_t>(sms) * 128 ? EVOGP_STRATEGY_INTRA : EVOGP_STRATEGY_INTER;
   const double lL = std::log(std::max(L, 1)), lP = std::log(static_cast<double>(std::max<int64_t>(P, 1))),
                lD = std::log(static_cast<double>(std::max<int64_t>(D, 1)));
-  const bool multi = n_out > 1;
+  // full-set single-output rows (tuning full_set) run the multi-output loop's
+  // code, so they take the multi-output cells: with one warp per tree the
+  // larger loop thrashes the instruction cache (c5b kernel (a): 53% of stalls
+  // "no instructions", 1.0e12 vs 3.0e12 GPops/s on kernel (b))
+  const bool multi = n_out > 1 || tuning().full_set != 0;
   int best = EVOGP_STRATEGY_INTER;
   double bd = 1e300;
   for (const SelectorEntry& e : kSelectorTable) {

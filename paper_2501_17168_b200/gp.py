@@ -10,6 +10,7 @@ defaults). All randomness is the counter-based draw of DESIGN.md R16.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from dataclasses import dataclass, field
 
@@ -188,8 +189,17 @@ class Evolution:
         generate(P, cfg, seed, device=dev, out=self.bufs[0])
         self.fitness = torch.empty(P, dtype=torch.float64, device=dev)
         self.generation = 0
+        # a function set beyond the paper's: the full-set kernel variants
+        # (evogp_tuning.full_set, include/evogp.h)
+        self._full_set = bool(set(cfg.funcs) - set(PAPER_FUNCS))
         if strategy == "auto":
-            self.strategy = selector_strategy(self.bufs[0], int(X.shape[0]))
+            with self._hint():
+                self.strategy = selector_strategy(self.bufs[0], int(X.shape[0]))
+
+    def _hint(self):
+        from . import tuning_hint
+
+        return tuning_hint(full_set=True) if self._full_set else contextlib.nullcontext()
 
     @property
     def population(self):
@@ -197,7 +207,8 @@ class Evolution:
 
     def evaluate(self):
         t, v, s = self.population
-        self._sr(t, v, s, self.X, self.y, strategy=self.strategy, out=self.fitness)
+        with self._hint():
+            self._sr(t, v, s, self.X, self.y, strategy=self.strategy, out=self.fitness)
         return self.fitness
 
     def step(self):

@@ -956,8 +956,8 @@ def test_paired_edge_cases():
                           device="cuda"), torch.zeros((1, n_in), device="cuda"))
 
 
-@pytest.mark.parametrize("reorder", [True, False])
-def test_long_rows_evolved_shapes(reorder):
+@pytest.mark.parametrize("reorder,full_set", [(True, False), (False, False), (True, True), (False, True)])
+def test_long_rows_evolved_shapes(reorder, full_set):
     """max_len 512 (tab:sr_params P:475): generated GROW/FULL populations with
     deep, unbalanced trees and 256-deep left combs, IEEE mix, both kernels,
     with the compile pass's reordering on (shared stacks) and off (the global
@@ -982,7 +982,7 @@ def test_long_rows_evolved_shapes(reorder):
     X = synth.dataset_X(12, 0, D, n_in, lo=0.5, hi=1.5)
     r32 = oracle.evaluate(t, v, s, X, mode=1)[:, :, 0]
     dev = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (t, v, s)]
-    with tuning(no_reorder=not reorder):
+    with tuning(no_reorder=not reorder, full_set=full_set):
         for strategy in ("inter", "intra"):
             g = gpu_eval(dev, X, 1, strategy)[:, :, 0]
             assert same_bits_mod_zero(g, r32).all(), strategy
@@ -1007,8 +1007,10 @@ def test_inconsistent_sizes_skip_reordering():
     for sizes in (s, s_bad):
         dev = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (t, v, sizes)]
         for strategy in ("inter", "intra"):
-            g = gpu_eval(dev, X, 1, strategy)[:, :, 0]
-            assert same_bits_mod_zero(g, r32).all(), strategy
+            for full_set in (False, True):
+                with tuning(full_set=full_set):
+                    g = gpu_eval(dev, X, 1, strategy)[:, :, 0]
+                assert same_bits_mod_zero(g, r32).all(), (strategy, full_set)
 
 
 def test_multi_output_deep_rows_multipass():

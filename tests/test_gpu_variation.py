@@ -247,6 +247,28 @@ def test_evolution_runs_and_improves():
     assert (rs == s).all()
 
 
+def test_evolution_full_function_set_hint():
+    """An Evolution over a function set beyond the paper's evaluates on the
+    full-set kernel variants (tuning_hint(full_set=True) around its calls):
+    fitness identical to the bit to a default-tuned sr_fitness of the same
+    population, and the thread's tuning is left as it was."""
+    e = _e()
+    L, P, D = 63, 2048, 300
+    cfg = e.GPConfig(max_len=L, n_inputs=2, funcs=tuple(range(22)), p_mutation=0.2)
+    X = synth.dataset_X(9, 0, D, 2, "uniform", -5.0, 5.0)
+    y = synth.pagie_y(X)
+    Xd, yd = torch.from_numpy(X).to(DEV), torch.from_numpy(y).to(DEV)
+    ev = e.Evolution(P, cfg, Xd, yd, seed=4)
+    assert ev._full_set
+    for _ in range(3):
+        ev.step()
+    f = ev.evaluate().clone()
+    t, v, s = ev.population
+    g = e.sr_fitness(t, v, s, Xd, yd, strategy=ev.strategy)
+    assert torch.equal(f.view(torch.int64), g.view(torch.int64))
+    assert not e._TUNING.kw["full_set"]
+
+
 def test_full_size_loop_population_fitness_sampled():
     """g1 at full size (P = 10^5, max_len 512, D = 392, the bench's
     configuration): after 10 device generations, the fused fitness of 300
