@@ -177,9 +177,9 @@ __device__ __forceinline__ u64 tan_full2(u64 x) {  // fm_tan_fast per point
 #include "hot_ptx.inc"
 
 // Multi-output rows (Modi, reading R4) at K = 4 or 8: the inline-PTX
-// loop (hot_ptx.inc) runs every node except the four functions with CUDA
-// libm bodies; at one of those it returns the node (esc = its hot code,
-// ew0 = its word, pn / top advanced) and this loop applies the library
+// loop (hot_ptx.inc) runs every node except pow (CUDA libm body) and trig
+// with a point beyond 2^40; at one of those it returns the node (esc = its
+// hot code, ew0 = its word, pn / top advanced) and this loop applies the
 // function — the same code as every other copy — with the Modi epilogue,
 // then re-enters. accl: the lane's Modi accumulators (slot stride 32 K).
 template <int K>
@@ -247,11 +247,7 @@ __device__ __forceinline__ bool interp_multi(const Node* __restrict__ tree, int 
     _Pragma("unroll") for (int k = 0; k < K - 1; ++k) a[k] = a[k + 1]; \
     a[K - 1] = v;                                                 \
   }
-      if (c == HC_EXP) {
-        EVOGP_ROT(expf)
-      } else if (c == HC_TANH) {
-        EVOGP_ROT(tanhf)
-      } else if (c == HC_SIN) {  // trig with a point beyond 2^40 (the loop's table-free range)
+      if (c == HC_SIN) {  // trig with a point beyond 2^40 (the loop's table-free range)
         EVOGP_ROT(fm_sin_ext)
       } else if (c == HC_COS) {
         EVOGP_ROT(fm_cos_ext)
@@ -476,8 +472,8 @@ __device__ __forceinline__ bool interp_hot(const Node* __restrict__ tree, int le
             SCALAR_BIN(HC_LE, hot_le)
             SCALAR_BIN(HC_GE, hot_ge)
             SCALAR_UN(HC_LOG, fn_plog)
-            SCALAR_UN(HC_EXP, expf)
-            SCALAR_UN(HC_TANH, tanhf)
+            SCALAR_UN(HC_EXP, fm_exp)
+            SCALAR_UN(HC_TANH, fm_tanh)
             UN_CASES(HC_NEG, { FOR2 t[j] = mul2(t[j], splat(-1.0f)); })
             SCALAR_UN(HC_ABS, fabsf)
             UN_CASES(HC_SQRT, {

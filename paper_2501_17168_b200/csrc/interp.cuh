@@ -217,8 +217,8 @@ static __device__ __noinline__ float fold_unary(int f, float c) {
     case F_COS: return a <= kFltMax ? fm_cos_ext(c) : slow_cosf(c);
     case F_TAN: return a <= kFltMax ? fm_tan_ext(c) : slow_tanf(c);
     case F_LOG: return fn_plog(c);
-    case F_EXP: return expf(c);
-    case F_TANH: return tanhf(c);
+    case F_EXP: return fm_exp(c);
+    case F_TANH: return fm_tanh(c);
     case F_NEG: return -c;
     case F_ABS: return a;
     case F_SQRT: return a == 0.0f ? 0.0f : ((a <= kSqrtRange && a >= kSqrtRangeMin) ? sqrt_fast(a) : slow_sqrt(a));
@@ -473,8 +473,8 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
     break;                                                                   \
   }
       UN_ROT(F_LOG, fn_plog)
-      UN_ROT(F_EXP, expf)
-      UN_ROT(F_TANH, tanhf)
+      UN_ROT(F_EXP, fm_exp)
+      UN_ROT(F_TANH, fm_tanh)
       UN(F_NEG, -a)
       UN(F_ABS, fabsf(a))
       case OP_FN + F_SQRT: {  // sqrt(|a|)

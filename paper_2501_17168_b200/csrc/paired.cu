@@ -55,8 +55,8 @@ __device__ __forceinline__ float apply_fn(int f, float a, float b, float c) {
     case F_MIN: return fminf(a, b);
     case F_POW: return powf(fabsf(a), b);
     case F_LOG: return fabsf(a) > kDelta ? fm_log(fabsf(a)) : 0.0f;
-    case F_EXP: return expf(a);
-    case F_TANH: return tanhf(a);
+    case F_EXP: return fm_exp(a);
+    case F_TANH: return fm_tanh(a);
     case F_NEG: return -a;
     case F_ABS: return fabsf(a);
     case F_SQRT: {
