@@ -1,6 +1,6 @@
 # usage: bash tools/gpu_profile.sh TAG [configs]  — ncu launch lists + full captures of the dominant kernels
 TAG=${1:-r01}; shift
-CONFIGS=${@:-c2 c3 c4 c5 n2}
+CONFIGS=${@:-c2 c3 c4 c5 c5b n2}
 mkdir -p gpurun_out
 kern() { case $1 in n2) echo k_paired;; *) echo "k_in(ter|tra)";; esac; }  # the eval kernel the selector picks
 for c in $CONFIGS; do

@@ -1,7 +1,7 @@
 # usage: bash tools/gpu_results.sh TAG — one full bench line per config (with e2e and cpu_baseline)
 TAG=${1:-r01}
 mkdir -p gpurun_out/results_$TAG
-for c in c2 c3 c4 c5 n2; do
+for c in c1 c2 c3 c4 c5 c5b n2; do
   timeout 600 python bench.py --config $c --steps 20 --warmup 5 > gpurun_out/results_$TAG/$c.json 2> gpurun_out/results_$TAG/$c.err
 done
 timeout 600 python bench.py --config g1 --steps 100 --warmup 3 > gpurun_out/results_$TAG/g1.json 2> gpurun_out/results_$TAG/g1.err

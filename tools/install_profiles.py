@@ -33,7 +33,7 @@ def launch_stats(path):
 
 
 names = {}
-for c in ["c2", "c3", "c4", "c5", "n2"]:
+for c in ["c2", "c3", "c4", "c5", "c5b", "n2"]:
     # named after the kernel the capture holds (the selector's choice), as bench.py looks it up
     d = json.load(open(f"{R}/prof_{c}_{TAG}.json"))
     kind = "paired" if "k_paired" in d["kernel"] else ("intra" if "k_intra" in d["kernel"] else "inter")
@@ -50,7 +50,7 @@ for k in ["k_eval", "k_prepare", "k_reproduce"]:
     json.dump(d, open(f"profiles/ncu_g1_{k}_summary.json", "w"), indent=1)
 shutil.copy(f"gpurun_out/launches_g1_{TAG}.csv", f"profiles/launches_g1_{TAG}.csv")
 os.makedirs(f"profiles/results_{TAG}", exist_ok=True)
-for c in ["c2", "c3", "c4", "c5", "n2", "g1"]:
+for c in ["c1", "c2", "c3", "c4", "c5", "c5b", "n2", "g1"]:
     shutil.copy(f"gpurun_out/results_{TAG}/{c}.json", f"profiles/results_{TAG}/{c}.json")
 for c in names:
     d = json.load(open("profiles/" + names[c]))
