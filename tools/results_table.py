@@ -4,7 +4,7 @@ import json, os, sys
 src = sys.argv[1]
 rows = ["| Config | value (GPops/s) | strategy | kernel (GPops/s) | roof frac | e2e (GPops/s) | oracle (GPops/s, cores) | notes |",
         "|---|---|---|---|---|---|---|---|"]
-for c in ("c3", "c2", "c4", "c5", "c1", "g1", "n2"):
+for c in ("c3", "c2", "c4", "c5", "c5b", "c1", "g1", "n2"):
     p = os.path.join(src, f"bench_{c}.json") if os.path.isdir(src) else f"gpurun_out/bench_{c}_{src}.json"
     if os.path.isdir(src) and not os.path.exists(p):
         p = os.path.join(src, f"{c}.json")
