@@ -177,11 +177,10 @@ __device__ __forceinline__ u64 tan_full2(u64 x) {  // fm_tan_fast per point
 #include "hot_ptx.inc"
 
 // Multi-output rows (Modi, reading R4) at K = 4 or 8: the inline-PTX
-// loop (hot_ptx.inc) runs every node except pow (CUDA libm body) and trig
-// with a point beyond 2^40; at one of those it returns the node (esc = its
-// hot code, ew0 = its word, pn / top advanced) and this loop applies the
-// function — the same code as every other copy — with the Modi epilogue,
-// then re-enters. accl: the lane's Modi accumulators (slot stride 32 K).
+// loop (hot_ptx.inc) runs every node except trig with a point beyond 2^40
+// (the table tier); at such a node it returns (esc = its hot code, ew0 = its
+// word, pn / top advanced) and this loop applies the function — the same
+// code as every other copy — with the Modi epilogue, then re-enters. accl: the lane's Modi accumulators (slot stride 32 K).
 template <int K>
 __device__ __forceinline__ bool interp_multi(const Node* __restrict__ tree, int len, const float* __restrict__ xl,
                                              float* stk, float* accl, float (&out)[K]) {
@@ -217,26 +216,7 @@ __device__ __forceinline__ bool interp_multi(const Node* __restrict__ tree, int 
     float a[K], rt[K];
 #pragma unroll
     for (int j = 0; j < N2; ++j) unpk(t[j], a[2 * j], a[2 * j + 1]);
-    if (c == HC_POW || c == HC_POWR) {  // pow(|a|, b), b popped (the rightmost child); POW_R: pow(|b|, a)
-      const bool rev = c == HC_POWR;
-      top -= SLOT * 4;
-      vld<K>(stk + (top - top0) / 4, rt);
-      float e[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) e[k] = rt[k];
-#pragma unroll 1
-      for (int it = 0; it < K; ++it) {  // one inlined powf body, register rotation
-        const float v = powf(fabsf(rev ? e[0] : a[0]), rev ? a[0] : e[0]);
-        const float e0 = e[0];
-#pragma unroll
-        for (int k = 0; k < K - 1; ++k) {
-          a[k] = a[k + 1];
-          e[k] = e[k + 1];
-        }
-        a[K - 1] = v;
-        e[K - 1] = e0;
-      }
-    } else {  // unary: the operand is the rightmost child
+    {  // trig with a point beyond 2^40 (unary: the operand is the rightmost child)
 #pragma unroll
       for (int k = 0; k < K; ++k) rt[k] = a[k];
       // one branch per function (warp-uniform), each one inlined body applied
@@ -247,7 +227,7 @@ __device__ __forceinline__ bool interp_multi(const Node* __restrict__ tree, int 
     _Pragma("unroll") for (int k = 0; k < K - 1; ++k) a[k] = a[k + 1]; \
     a[K - 1] = v;                                                 \
   }
-      if (c == HC_SIN) {  // trig with a point beyond 2^40 (the loop's table-free range)
+      if (c == HC_SIN) {
         EVOGP_ROT(fm_sin_ext)
       } else if (c == HC_COS) {
         EVOGP_ROT(fm_cos_ext)

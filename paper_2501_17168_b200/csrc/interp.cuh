@@ -191,8 +191,8 @@ __device__ __forceinline__ float fn_plog(float a) { return fabsf(a) > kDelta ? f
 
 // element forms shared by the packed interpreter (hot.cuh): the same
 // expressions as interpret's cases (reading R3)
-__device__ __forceinline__ float hot_pow(float a, float b) { return powf(fabsf(a), b); }
-__device__ __forceinline__ float hot_powr(float a, float b) { return powf(fabsf(b), a); }
+__device__ __forceinline__ float hot_pow(float a, float b) { return fm_pow(a, b); }
+__device__ __forceinline__ float hot_powr(float a, float b) { return fm_pow(b, a); }
 __device__ __forceinline__ float hot_lt(float a, float b) { return a < b ? 1.0f : 0.0f; }
 __device__ __forceinline__ float hot_gt(float a, float b) { return a > b ? 1.0f : 0.0f; }
 __device__ __forceinline__ float hot_le(float a, float b) { return a <= b ? 1.0f : 0.0f; }
@@ -422,7 +422,7 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
       UN_RANGED(F_TAN, kFltMax, fm_tan_ext, slow_tanf(a), kTanSmall, fm_tan_small)
       BIN(F_MAX, fmaxf(a, bb))
       BIN(F_MIN, fminf(a, bb))
-// pow(|BASE|, EXPO): one inlined powf body applied to the K points by
+// pow(|BASE|, EXPO): one inlined fm_pow body applied to the K points by
 // register rotation (static indices, no K-fold code duplication)
 #define POW_CASE(OPC, BASE, EXPO)          \
   case OPC: {                              \
@@ -433,7 +433,7 @@ __device__ __forceinline__ bool interpret(const Node* __restrict__ tree, int len
       e[k] = EXPO[k];                      \
     }                                      \
     _Pragma("unroll 1") for (int it = 0; it < K; ++it) { \
-      const float v = powf(fabsf(a[0]), e[0]); \
+      const float v = fm_pow(a[0], e[0]);  \
       const float e0 = e[0];               \
       _Pragma("unroll") for (int k = 0; k < K - 1; ++k) { \
         a[k] = a[k + 1];                   \

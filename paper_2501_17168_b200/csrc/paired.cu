@@ -53,7 +53,7 @@ __device__ __forceinline__ float apply_fn(int f, float a, float b, float c) {
     case F_TAN: return fabsf(a) <= kFltMax ? fm_tan_ext(a) : slow_tanf(a);
     case F_MAX: return fmaxf(a, b);
     case F_MIN: return fminf(a, b);
-    case F_POW: return powf(fabsf(a), b);
+    case F_POW: return fm_pow(a, b);
     case F_LOG: return fabsf(a) > kDelta ? fm_log(fabsf(a)) : 0.0f;
     case F_EXP: return fm_exp(a);
     case F_TANH: return fm_tanh(a);
