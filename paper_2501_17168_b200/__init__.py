@@ -319,16 +319,18 @@ def check_device_flags(workspace: Workspace, stream=None) -> int:
 
 
 def set_tuning(target_warps: int = 0, no_reorder: bool = False, no_fuse: bool = False, K: int = 0,
-               reorder_above: int = 0, unit_chunks: int = 0, full_set: bool = False) -> None:
+               reorder_above: int = 0, unit_chunks: int = 0, full_set: bool = False,
+               fused_compile: bool = False) -> None:
     """evogp_set_tuning for this thread (calibration sweeps, tests); all
     defaults = the library's own plan. Results never depend on it."""
     t = _lib.Tuning(int(target_warps), int(bool(no_reorder)), int(bool(no_fuse)), int(K), int(reorder_above),
-                    int(unit_chunks), int(bool(full_set)))
+                    int(unit_chunks), int(bool(full_set)), int(bool(fused_compile)))
     st = _LIB.evogp_set_tuning(ctypes.byref(t))
     if st != OK:
         raise EvogpError(st, "evogp_set_tuning")
     _TUNING.kw = dict(target_warps=target_warps, no_reorder=no_reorder, no_fuse=no_fuse, K=K,
-                      reorder_above=reorder_above, unit_chunks=unit_chunks, full_set=full_set)
+                      reorder_above=reorder_above, unit_chunks=unit_chunks, full_set=full_set,
+                      fused_compile=fused_compile)
 
 
 _TUNING = threading.local()

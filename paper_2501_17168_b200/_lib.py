@@ -83,4 +83,5 @@ class Tuning(ctypes.Structure):
     """evogp_tuning (include/evogp.h): launch-plan overrides, 0 = default."""
     _fields_ = [("target_warps", ctypes.c_int32), ("no_reorder", ctypes.c_int32), ("no_fuse", ctypes.c_int32),
                 ("K", ctypes.c_int32), ("reorder_above", ctypes.c_int32),
-                ("unit_chunks", ctypes.c_int32), ("full_set", ctypes.c_int32)]
+                ("unit_chunks", ctypes.c_int32), ("full_set", ctypes.c_int32),
+                ("fused_compile", ctypes.c_int32)]

@@ -15,7 +15,7 @@ thread_local char t_last_error[512] = "no error";
 thread_local int32_t t_last_launches = 0;
 thread_local void* t_ev_start = nullptr;
 thread_local void* t_ev_end = nullptr;
-thread_local evogp_tuning t_tuning = {0, 0, 0, 0, 0, 0, 0};
+thread_local evogp_tuning t_tuning = {0, 0, 0, 0, 0, 0, 0, 0};
 
 int current_device() {
   int dev = 0;
@@ -239,7 +239,7 @@ extern "C" int evogp_set_kernel_timing(void* start_event, void* end_event) {
 
 extern "C" int evogp_set_tuning(const evogp_tuning* t) {
   if (!t) {
-    t_tuning = evogp_tuning{0, 0, 0, 0, 0, 0, 0};
+    t_tuning = evogp_tuning{0, 0, 0, 0, 0, 0, 0, 0};
     return EVOGP_OK;
   }
   if (t->target_warps < 0 || t->target_warps > 64) return fail(EVOGP_E_ARG, "target_warps out of range");

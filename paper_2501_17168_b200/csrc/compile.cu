@@ -324,10 +324,11 @@ __device__ int fuse_copy(const Node* prog, int n, Node* row, int lane) {
 }
 
 // Compile one row with the whole warp (decode / validate, reorder when deeper
-// than the evaluation kernel's shared stack, fuse leaves, hot codes), using
-// `scratch` sized for rows of up to Lc nodes (the row is at most that long).
-__device__ void compile_row_warp(const KParams& p, int64_t tp, unsigned char* scratch, int Lc, int lane) {
-  Node* row = p.prog + tp * p.prog_ld;
+// than the evaluation kernel's shared stack, fuse leaves, hot codes) into
+// `row` (global or shared), using `scratch` sized for rows of up to Lc nodes
+// (the row is at most that long). A malformed row raises the device flag.
+__device__ __forceinline__ TreeInfo compile_row(const KParams& p, int64_t tp, Node* row, unsigned char* scratch,
+                                                int Lc, int lane) {
   TreeInfo ti;
   if (p.reorder_scratch_bytes > 0) {
     // decode into shared scratch; reorder when the row is deeper than the
@@ -371,11 +372,29 @@ __device__ void compile_row_warp(const KParams& p, int64_t tp, unsigned char* sc
     ti = stage_tree_warp(p, tp, row, lane, true);  // hot codes (multi-output rows: + Modi twins)
   }
 compiled:
-  if (lane == 0) {
-    p.info[tp] = TreeMeta{ti.len, ti.valid ? (ti.maxdepth | (ti.paper ? kPaperRow : 0)) : -1};
-    if (!ti.valid) atomicOr(&p.ctl->flags, 1);
-  }
+  if (lane == 0 && !ti.valid) atomicOr(&p.ctl->flags, 1);
   __syncwarp();
+  return ti;
+}
+
+__device__ void compile_row_warp(const KParams& p, int64_t tp, unsigned char* scratch, int Lc, int lane) {
+  const TreeInfo ti = compile_row(p, tp, p.prog + tp * p.prog_ld, scratch, Lc, lane);
+  if (lane == 0) p.info[tp] = TreeMeta{ti.len, ti.valid ? (ti.maxdepth | (ti.paper ? kPaperRow : 0)) : -1};
+  __syncwarp();
+}
+
+// kernel (a) compiling its own rows: the program goes straight into the
+// warp's shared buffer (no program-row round trip through HBM, no p.info)
+__device__ TreeInfo compile_row_smem(const KParams& p, int64_t tp, Node* row, unsigned char* scratch, int lane) {
+  return compile_row(p, tp, row, scratch, p.prep_cap, lane);
+}
+
+const void* kernel_inter_fused(int mode) {
+  switch (mode) {
+    case MODE_EVAL1: return reinterpret_cast<const void*>(&k_inter<8, MODE_EVAL1, false, true>);
+    case MODE_SSE: return reinterpret_cast<const void*>(&k_inter<8, MODE_SSE, false, true>);
+  }
+  return nullptr;
 }
 
 // ------------------------------------------------------------------------
@@ -414,7 +433,7 @@ __global__ void __launch_bounds__(256) k_prepare(const KParams p, const float* _
   const int64_t nwarps = stride >> 5;
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* scratch = smem + static_cast<size_t>(threadIdx.x >> 5) * p.reorder_scratch_bytes;
-  for (int64_t tp = t0 >> 5; tp < p.P; tp += nwarps) {
+  for (int64_t tp = t0 >> 5; tp < p.P && !p.fused_compile; tp += nwarps) {
     if (p.prep_cap < p.L) {
       // the long tier: rows longer than this kernel's scratch are queued (as
       // are malformed lengths, which the long tier flags)
@@ -486,10 +505,10 @@ void launch_prepare(const KParams& kp, int mode, const float* X, int32_t x_layou
   const int64_t total = static_cast<int64_t>(kp.n_in + 1) * kp.Dpad;
   // warps per CTA such that their compile scratch fits the opt-in shared memory
   constexpr int wpb_cap = 8;
-  const int wpb = kp.reorder_scratch_bytes > 0 ? std::max(1, std::min(wpb_cap, (220 * 1024) / kp.reorder_scratch_bytes))
-                                               : wpb_cap;
+  const int scr = kp.fused_compile ? 0 : kp.reorder_scratch_bytes;  // fused: X staging only
+  const int wpb = scr > 0 ? std::max(1, std::min(wpb_cap, (220 * 1024) / scr)) : wpb_cap;
   const int threads = 32 * wpb;
-  const size_t psmem = static_cast<size_t>(wpb) * kp.reorder_scratch_bytes;
+  const size_t psmem = static_cast<size_t>(wpb) * scr;
   if (psmem > 48 * 1024) {
     static thread_local int attr_dev = -1;
     int dev = 0;
@@ -499,8 +518,9 @@ void launch_prepare(const KParams& kp, int mode, const float* X, int32_t x_layou
       attr_dev = dev;
     }
   }
+  const int64_t rows_per = kp.fused_compile ? 0 : (kp.P + wpb - 1) / wpb;
   const int64_t blocks = std::max<int64_t>(
-      1, std::min<int64_t>(std::max((total + threads - 1) / threads, (kp.P + wpb - 1) / wpb),
+      1, std::min<int64_t>(std::max((total + threads - 1) / threads, rows_per),
                            static_cast<int64_t>(kp.sms) * 16 * (8 / wpb)));
   k_prepare<<<static_cast<int>(blocks), threads, psmem, s>>>(kp, X, x_layout, mode_reduce(mode) ? y : nullptr,
                                                             mode == MODE_CLS);

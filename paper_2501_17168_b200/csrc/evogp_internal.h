@@ -180,6 +180,10 @@ struct KParams {
   // one tier)
   int32_t prep_cap;
   int32_t long_scratch_bytes;
+  // kernel (a) compiles its own rows (every tree one work unit): k_prepare
+  // only stages X; the evaluation warp compiles into its shared program
+  // buffer, with its stack region as the compile scratch
+  int32_t fused_compile;
   double* partials;
   int32_t* long_rows;  // rows longer than prep_cap, compiled by k_prepare_long (P slots)
   Control* ctl;
@@ -229,6 +233,8 @@ const void* kernel_intra_k8(int mode);
 const void* kernel_intra_k16(int mode);
 // eval_full.cu: the full-set variants (single-output modes, K = 4 / 8)
 const void* kernel_full(int strategy, int K, int mode);
+// compile.cu: kernel (a) at K = 8 compiling its own rows (KParams::fused_compile)
+const void* kernel_inter_fused(int mode);
 
 // paired.cu
 int launch_paired(const int16_t* type, const float* value, const int16_t* size, int64_t P, int32_t L, int32_t ld,

@@ -922,13 +922,17 @@ __device__ __forceinline__ TreeInfo load_program_warp(const KParams& p, int64_t 
 // (a) inter-individual kernel
 // ------------------------------------------------------------------------
 
+// compile.cu: one row compiled by the warp straight into its shared program
+// buffer (kernel (a) with KParams::fused_compile; scratch = the warp's stack)
+__device__ TreeInfo compile_row_smem(const KParams& p, int64_t tp, Node* row, unsigned char* scratch, int lane);
+
 __device__ __forceinline__ long long next_ticket(const KParams& p, int lane) {
   unsigned long long t = 0;
   if (lane == 0) t = atomicAdd(&p.ctl->work, 1ull);
   return static_cast<long long>(__shfl_sync(FULL_MASK, t, 0));
 }
 
-template <int K, int MODE, bool FULL = false>
+template <int K, int MODE, bool FULL = false, bool COMPILE = false>
 __global__ void __launch_bounds__(32 * kInterWarps, (K >= 16 || (K == 8 && mode_multi(MODE))) ? 4 : 8)
     k_inter(const KParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -958,7 +962,11 @@ __global__ void __launch_bounds__(32 * kInterWarps, (K >= 16 || (K == 8 && mode_
     const int64_t tp = u - static_cast<int64_t>(g) * p.P;
     if (tp != staged) {
       __syncwarp();
-      ti = load_program_warp(p, tp, s_tree, lane);
+      if constexpr (COMPILE) {
+        ti = compile_row_smem(p, tp, s_tree, wbase + p.tree_bytes, lane);
+      } else {
+        ti = load_program_warp(p, tp, s_tree, lane);
+      }
       staged = tp;
     }
     const int c0 = g * p.ucs, c1 = min(p.nch, c0 + p.ucs);

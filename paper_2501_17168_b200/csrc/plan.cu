@@ -303,6 +303,16 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   kp.long_scratch_bytes = kp.prep_cap < L ? scratch_for(L) : 0;
   kp.fuse = fuse_on ? 1 : 0;
   kp.reorder_above = tu.reorder_above > 0 ? tu.reorder_above : SD;
+  // opt-in (tuning fused_compile): kernel (a) compiles its own rows when every
+  // tree is one work unit (no program-row round trip through HBM, no compile
+  // launch; the scratch is the warp's stack region). Not the default: on C4
+  // the kernel then holds the compile code and the interpreter loop, and
+  // stalls on instruction fetch (58% "no instruction"; 11.0 vs 4.1 + 2.1 ms)
+  kp.fused_compile = (strategy == EVOGP_STRATEGY_INTER && K == 8 && !multi &&
+                      (mode == MODE_SSE || mode == MODE_EVAL1) && ngrp == 1 && kp.prep_cap == L &&
+                      kp.reorder_scratch_bytes <= warp_smem && tu.full_set == 0 && tu.fused_compile != 0)
+                         ? 1
+                         : 0;
   kp.out_magic = static_cast<int32_t>((0x100000000ull + n_out - 1) / n_out);
   kp.deep_slots = deep_slots;
   kp.deep_slot_floats = deep_slot_floats;
@@ -325,9 +335,9 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   pl.off_deep_pw = off;
   off += round_up(static_cast<int64_t>(grid) * warps * kp.deep_pw_levels * 32 * K * 4, 256);
   pl.off_prog = off;
-  off += round_up(P * prog_ld * 8, 256);
+  off += kp.fused_compile ? 0 : round_up(P * prog_ld * 8, 256);
   pl.off_info = off;
-  off += round_up(P * 8, 256);
+  off += kp.fused_compile ? 0 : round_up(P * 8, 256);
   pl.total = off;
   return EVOGP_OK;
 }
@@ -344,7 +354,7 @@ int launch(Plan& pl, int mode, const float* X, int32_t x_layout, const float* y,
     launch_prepare_long(kp, s);
     ++launches;
   }
-  const void* fn = kernel_ptr(pl.strategy, pl.K, mode);
+  const void* fn = kp.fused_compile ? kernel_inter_fused(mode) : kernel_ptr(pl.strategy, pl.K, mode);
   if (!fn) return EVOGP_E_ARG;
   void* args[] = {&kp};
   if (ev_start) cudaEventRecord(static_cast<cudaEvent_t>(ev_start), s);

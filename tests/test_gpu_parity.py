@@ -246,6 +246,39 @@ def test_full_set_variant_bit_identical(strategy):
     assert ok.all(), (~ok).sum()
 
 
+@pytest.mark.parametrize("mix,L,D,reorder", [("paper", 127, 256, True), ("ieee", 127, 200, True),
+                                              ("paper", 63, 256, True), ("full", 127, 256, False)])
+def test_fused_compile_bit_identical(mix, L, D, reorder):
+    """Kernel (a) compiling its own rows (tuning fused_compile; every tree
+    one work unit, e.g. C4's D = 256) computes what it computes from the
+    compile pass's rows: outputs and fused MSEs identical to the bit with the fusion off,
+    over reordered / fused / deep and malformed rows; IEEE rows bit-exact to
+    the FP32-faithful oracle."""
+    evogp = _evogp()
+    P, n_in = 700, 8
+    pt, X, y = make_case(800 + D, P, L, n_in, D, mix)
+    dt = to_device(pt, L, n_in)
+    t, v, s = (a.clone() for a in dt)
+    t[5, 0] = 1  # root becomes a VAR: leftover operands (malformed: NaN + device flag)
+    v[5, 0] = 0
+    s[9, 0] = L + 1  # a length beyond max_len
+    dt = (t, v, s)
+    with tuning(no_reorder=not reorder, fused_compile=True):
+        a, ma = gpu_eval(dt, X, 1, "inter"), gpu_mse(dt, X, y, "inter")
+    with tuning(no_reorder=not reorder):
+        b, mb = gpu_eval(dt, X, 1, "inter"), gpu_mse(dt, X, y, "inter")
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert np.array_equal(ma.view(np.uint64), mb.view(np.uint64))
+    assert np.isnan(a[5]).all() and np.isnan(a[9]).all() and np.isnan(ma[[5, 9]]).all()
+    assert np.isfinite(ma).mean() > 0.5
+    if mix == "ieee":
+        ok = np.ones(P, bool)
+        ok[[5, 9]] = False
+        to, vo, so = oracle_arrays(pt, L, n_in)
+        r32 = oracle.evaluate(to[ok], vo[ok], so[ok], X, mode=1)[:, :, 0]
+        assert same_bits_mod_zero(a[ok, :, 0], r32).all()
+
+
 def test_determinism():
     pt, X, y = make_case(500, 500, 63, 4, 4096, "paper")
     dt = to_device(pt, 63, 4)
