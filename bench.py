@@ -632,12 +632,12 @@ def main():
         modi_nonzero = float((out_eval != 0).flatten(0, -3).any(dim=-2).float().mean().item()) if out_eval.dim() == 3 else None
     value = total_work * args.steps / (step_ms * 1e-3)
 
-    # ---- launch-bound configs (c1): the same step replayed from a CUDA graph
-    # (SURVEY §8(d) config 1): G steps captured once, the graph replayed K
-    # times; value = G * K * work / device time of the replays
+    # ---- launch-bound configs (c1; c2's 0.1 ms step): the same step replayed
+    # from a CUDA graph: G steps captured once, the
+    # graph replayed K times; value = G * K * work / device time of the replays
     graph = None
-    if cfg.index == 1 and world == 1 and not cfg.paired:
-        G = 100
+    if cfg.index in (1, 2) and world == 1 and not cfg.paired and not evalcfg:
+        G = 100 if cfg.index == 1 else 20
         gs = torch.cuda.Stream(device=dev)
         gs.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(gs):
@@ -661,7 +661,7 @@ def main():
         graph = {"value": total_work * G * args.steps / (gms * 1e-3), "unit": UNIT, "steps_per_graph": G,
                  "replays": args.steps, "us_per_step": gms * 1e3 / (G * args.steps),
                  "note": "CUDA-graph-batched replay of the same step (launch-bound config); the graph's kernels "
-                         "are the same two launches per step, no L2 flush between graph steps"}
+                         "are the same launches per step, no L2 flush between graph steps"}
 
     # ---- e2e: host prefix lists -> tensorize -> H2D -> device call -> D2H
     e2e = None
