@@ -10,6 +10,11 @@
                             per-warp global stacks, locked pool)
   Modi / classification   (multi-output store, argmax epilogue)
   k_paired, tensorize_device, generate / reproduce / exchange / tournament
+  full-set kernel variants  (tuning full_set: the packed multi loop on
+                            single-output rows, exp / tanh / pow in the loop)
+  fused compile             (tuning fused_compile: kernel (a) compiling its
+                            own rows into shared memory)
+  two-tier compile          (max_len 512: k_prepare_long)
 
 Sizes are tiny (sanitizers replay every access); the values are checked
 loosely against the oracle so a sanitizer-induced misbehaviour shows too.
@@ -56,6 +61,29 @@ def main():
             check_close(g, r64, (mix, strat))
             m = evogp.sr_fitness(t, v, s, Xd, yd, strategy=strat).cpu().numpy()
             assert np.isfinite(m).mean() > 0.5
+    # full-set kernel variants and the fused compile, single output (K = 8 / 4)
+    P, L, n_in, D = 64, 63, 3, 600
+    pt = synth.trees(21, 0, P, L, synth.M_FULL, n_in)
+    X = synth.dataset_X(21, 0, D, n_in, "normal")
+    y = synth.pagie_y(X)
+    (t, v, s), host = dev_trees(pt, L, n_in)
+    Xd, yd = torch.from_numpy(X).to(dev), torch.from_numpy(y).to(dev)
+    base = evogp.eval(t, v, s, Xd, strategy="intra").cpu().numpy()
+    for kw in (dict(full_set=True), dict(full_set=True, K=4), dict(fused_compile=True)):
+        evogp.set_tuning(**kw)
+        Dk = 256 if "fused_compile" in kw else D  # one work unit per tree
+        for strat in ("inter", "intra"):
+            g = evogp.eval(t, v, s, Xd[:Dk].contiguous(), strategy=strat).cpu().numpy()
+            assert np.array_equal(g.view(np.uint32), base[:, :Dk].view(np.uint32)), (kw, strat)
+            evogp.sr_fitness(t, v, s, Xd[:Dk].contiguous(), yd[:Dk].contiguous(), strategy=strat)
+    evogp.set_tuning()
+    # two-tier compile: max_len 512 with rows beyond the first tier's 192 nodes
+    gc = evogp.GPConfig(max_len=512, n_inputs=3, n_outputs=1, funcs=tuple(synth.M_PAPER), depth_min=6,
+                        depth_max=9)
+    pop = evogp.generate(48, gc, 5, device=dev)
+    Xd = torch.from_numpy(synth.dataset_X(22, 0, 300, 3)).to(dev)
+    for strat in ("inter", "intra"):
+        evogp.sr_fitness(*pop, Xd, Xd[:, 0].contiguous(), strategy=strat)
     # deep rows (left combs), reordering off: multi-pass / per-warp global / locked pool
     L, n_in, P, D = 127, 2, 12, 700
     offs, tys, vas = [0], [], []
