@@ -279,6 +279,26 @@ def test_fused_compile_bit_identical(mix, L, D, reorder):
         assert same_bits_mod_zero(a[ok, :, 0], r32).all()
 
 
+@pytest.mark.parametrize("n_out,full_set", [(3, False), (1, True)])
+def test_slow_path_extreme_operands_bitexact(n_out, full_set):
+    """Division, 1/x and sqrt with finite operands far beyond their fast
+    ranges (|x| up to 1e36, down to 1e-36): the multi-output / full-set PTX
+    loop evaluates such nodes in FP64 rounded once (correctly rounded, no
+    cold re-run) — bit-exact to the FP32-faithful oracle on the IEEE mix."""
+    P, L, n_in, D = 300, 63, 4, 2048
+    pt = synth.trees(77, 0, P, L, synth.MIXES["ieee"], n_in, n_out, 0.2 if n_out > 1 else 0.0)
+    rng = np.random.default_rng(77)
+    X = (np.sign(rng.standard_normal((D, n_in))) * 10.0 ** rng.uniform(-36, 36, (D, n_in))).astype(np.float32)
+    dt = to_device(pt, L, n_in, n_out)
+    t, v, s = oracle_arrays(pt, L, n_in, n_out)
+    r32 = oracle.evaluate(t, v, s, X, n_out=n_out, mode=1)
+    for strategy in ("inter", "intra"):
+        with tuning(full_set=full_set):
+            g = gpu_eval(dt, X, n_out, strategy)
+        ok = same_bits_mod_zero(g, r32)
+        assert ok.all(), (strategy, (~ok).sum())
+
+
 def test_determinism():
     pt, X, y = make_case(500, 500, 63, 4, 4096, "paper")
     dt = to_device(pt, 63, 4)
