@@ -193,3 +193,43 @@ def test_gp_config_zero_weights_rejected_only_with_mutation():
     c = GPConfig(max_len=63, n_inputs=4, mutation_weights=(0,) * 8, p_mutation=0.1).c()
     assert lib.evogp_reproduce(null, null, null, 10, 63, null, 10, 0, ctypes.byref(c), 1, null, null, null, null,
                                null, null) == _lib.E_ARG
+
+
+def test_tuning_struct_layout_matches_header(tmp_path):
+    """The ctypes mirror of evogp_tuning (_lib.Tuning) has the C header's size
+    and field offsets (compiled with gcc from include/)."""
+    fields = [f for f, _ in _lib.Tuning._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text("#include <stdio.h>\n#include <stddef.h>\n#include \"evogp.h\"\nint main(void){\n"
+                   "printf(\"%zu\\n\", sizeof(evogp_tuning));\n" +
+                   "".join(f"printf(\"%zu\\n\", offsetof(evogp_tuning, {f}));\n" for f in fields) +
+                   "return 0;}\n")
+    exe = tmp_path / "layout"
+    import subprocess
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    out = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    assert out[0] == ctypes.sizeof(_lib.Tuning)
+    assert out[1:] == [getattr(_lib.Tuning, f).offset for f in fields]
+
+
+def test_tuning_hint_nests_and_restores():
+    """tuning_hint overrides fields for a with-block on top of the thread's
+    tuning and restores it; the plan sees it (fused_compile drops the
+    program-row section of the workspace: every tree one work unit here)."""
+    args = (100_000, 256, 127, 8, 1)
+    evogp.set_tuning()
+    base = evogp.workspace_size(*args)
+    try:
+        evogp.set_tuning(unit_chunks=2)
+        with evogp.tuning_hint(fused_compile=True):
+            assert evogp._TUNING.kw["unit_chunks"] == 2 and evogp._TUNING.kw["fused_compile"]
+            fused = evogp.workspace_size(*args)
+            with evogp.tuning_hint(full_set=True):
+                assert evogp._TUNING.kw["fused_compile"] and evogp._TUNING.kw["full_set"]
+            assert not evogp._TUNING.kw["full_set"]
+        assert evogp._TUNING.kw == dict(target_warps=0, no_reorder=False, no_fuse=False, K=0, reorder_above=0,
+                                        unit_chunks=2, full_set=False, fused_compile=False)
+        assert fused < base
+    finally:
+        evogp.set_tuning()
+    assert evogp.workspace_size(*args) == base
