@@ -322,6 +322,8 @@ def run_loop(args, cfg):
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
+    if args.tune:
+        evogp.set_tuning(**{k: int(v) for k, v in (kv.split("=") for kv in args.tune.split(","))})
     gp = loop_gp_config(cfg)
     X, y = synth.config_data(cfg)
     Xd, yd = torch.from_numpy(X).to(dev), torch.from_numpy(y).to(dev)
