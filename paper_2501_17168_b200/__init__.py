@@ -12,6 +12,7 @@ P:221-258): ``type`` int16, ``value`` float32, ``size`` int16, each P x ld.
 from __future__ import annotations
 
 import contextlib
+import math
 import ctypes
 import threading
 
@@ -155,6 +156,17 @@ def _stream_ptr(stream, device):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+def _device_guard(device):
+    """Make `device` current for the body (the library plans and launches on
+    the current device); a no-op when it already is (the common case: a
+    context manager switch costs microseconds on launch-bound calls)."""
+    import torch
+
+    if device.index is None or device.index == torch.cuda.current_device():
+        return contextlib.nullcontext()
+    return torch.cuda.device(device)
+
+
 def _tree_args(type_, value, size, max_len):
     import torch
 
@@ -185,8 +197,8 @@ def _x_args(X, x_layout):
 
 def _check_out(out, shape, dtype, device):
     if out.dtype != dtype or not out.is_cuda or not out.is_contiguous() or out.device != device \
-            or out.numel() != int(np.prod(shape)):
-        raise ValueError(f"out must be a contiguous {dtype} CUDA tensor of {int(np.prod(shape))} elements on {device}")
+            or out.numel() != math.prod(shape):
+        raise ValueError(f"out must be a contiguous {dtype} CUDA tensor of {math.prod(shape)} elements on {device}")
 
 
 def eval(type_, value, size, X, n_outputs: int = 1, strategy="auto", x_layout="rowmajor", max_len=None,
@@ -199,7 +211,7 @@ def eval(type_, value, size, X, n_outputs: int = 1, strategy="auto", x_layout="r
     if out is None:
         out = torch.empty((P, D, n_outputs), dtype=torch.float32, device=X.device)
     _check_out(out, (P, D, n_outputs), torch.float32, X.device)
-    with torch.cuda.device(X.device):
+    with _device_guard(X.device):
         ws = _workspace(P, D, L, n_in, n_outputs, X.device, workspace, stream)
         st = _LIB.evogp_eval(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(X), D, n_in, lay, n_outputs,
                              _vp(out), STRATEGIES[strategy], ctypes.c_void_p(ws.ptr), ws.nbytes,
@@ -219,7 +231,7 @@ def _sr(fn, name, type_, value, size, X, y, strategy, x_layout, max_len, out, wo
     if out is None:
         out = torch.empty(P, dtype=torch.float64, device=X.device)
     _check_out(out, (P,), torch.float64, X.device)
-    with torch.cuda.device(X.device):
+    with _device_guard(X.device):
         ws = _workspace(P, D, L, n_in, 1, X.device, workspace, stream)
         st = fn(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(X), D, n_in, lay, _vp(y), _vp(out),
                 STRATEGIES[strategy], ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream, X.device))
@@ -256,7 +268,7 @@ def classification_accuracy(type_, value, size, X, labels, n_classes: int, strat
     if out is None:
         out = torch.empty(P, dtype=torch.float64, device=X.device)
     _check_out(out, (P,), torch.float64, X.device)
-    with torch.cuda.device(X.device):
+    with _device_guard(X.device):
         ws = _workspace(P, D, L, n_in, n_classes, X.device, workspace, stream)
         st = _LIB.evogp_classification_accuracy(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(X), D, n_in, lay,
                                                 n_classes, _vp(labels), _vp(out), STRATEGIES[strategy],
@@ -284,7 +296,7 @@ def eval_paired(type_, value, size, obs, n_outputs: int = 1, max_len=None, out=N
     if out is None:
         out = torch.empty(shape, dtype=torch.float32, device=obs.device)
     _check_out(out, shape, torch.float32, obs.device)
-    with torch.cuda.device(obs.device):
+    with _device_guard(obs.device):
         ws = workspace if workspace is not None else _flags_workspace(obs.device)
         st = _LIB.evogp_eval_paired(_vp(type_), _vp(value), _vp(size), P, L, ld, _vp(obs), B, n_in, n_outputs,
                                     _vp(out), ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream, obs.device))

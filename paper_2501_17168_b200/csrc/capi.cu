@@ -50,6 +50,48 @@ int check_common(const int16_t* type, const float* value, const int16_t* size, i
   return EVOGP_OK;
 }
 
+// The plan of a call depends only on its shape, mode, strategy, device and
+// the thread's tuning; launch-bound callers (C1: a 20-microsecond step) repeat
+// the same shape, so the last few plans are kept per thread (the selector's
+// nearest-cell search alone costs a few microseconds).
+struct PlanKey {
+  int64_t P, D;
+  int32_t L, n_in, n_out, mode, strategy, device;
+  evogp_tuning tu;
+};
+constexpr int kPlanCache = 8;
+thread_local PlanKey t_plan_keys[kPlanCache];
+thread_local Plan t_plans[kPlanCache];
+thread_local int t_plan_n = 0, t_plan_next = 0;
+
+int cached_plan(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_t n_out, int mode, int strategy,
+                int device) {
+  PlanKey k;
+  std::memset(&k, 0, sizeof(k));
+  k.P = P;
+  k.D = D;
+  k.L = L;
+  k.n_in = n_in;
+  k.n_out = n_out;
+  k.mode = mode;
+  k.strategy = strategy;
+  k.device = device;
+  k.tu = tuning();
+  for (int i = 0; i < t_plan_n; ++i) {
+    if (std::memcmp(&t_plan_keys[i], &k, sizeof(k)) == 0) {
+      pl = t_plans[i];
+      return EVOGP_OK;
+    }
+  }
+  const int st = plan_problem(pl, P, L, D, n_in, n_out, mode, strategy, device);
+  if (st != EVOGP_OK) return st;
+  t_plan_keys[t_plan_next] = k;
+  t_plans[t_plan_next] = pl;
+  t_plan_next = (t_plan_next + 1) % kPlanCache;
+  t_plan_n = std::min(t_plan_n + 1, kPlanCache);
+  return EVOGP_OK;
+}
+
 int run(int mode, const int16_t* type, const float* value, const int16_t* size, int64_t P, int32_t max_len,
         int32_t ld, const float* X, int64_t D, int32_t n_inputs, int32_t x_layout, int32_t n_outputs, float* out,
         const float* y, double* res, int div_by_D, int32_t strategy, void* workspace, size_t ws_bytes,
@@ -57,7 +99,7 @@ int run(int mode, const int16_t* type, const float* value, const int16_t* size, 
   t_last_launches = 0;
   if (strategy < EVOGP_STRATEGY_AUTO || strategy > EVOGP_STRATEGY_INTRA) return fail(EVOGP_E_ARG, "bad strategy");
   Plan pl;
-  int st = plan_problem(pl, P, max_len, D, n_inputs, n_outputs, mode, strategy, current_device());
+  int st = cached_plan(pl, P, max_len, D, n_inputs, n_outputs, mode, strategy, current_device());
   if (st != EVOGP_OK) return fail(st, "no launch plan for this shape");
   if (ws_bytes < pl.total) {
     char buf[160];
