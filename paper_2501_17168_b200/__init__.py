@@ -137,7 +137,9 @@ def _workspace(P, D, L, n_in, n_out, device, ws, stream=None):
     import torch
 
     s = stream if stream is not None else torch.cuda.current_stream(device)
-    key = (P, D, L, n_in, n_out, str(device), int(s.cuda_stream), threading.get_ident())
+    # the plan (and so the workspace size) depends on the thread's tuning
+    tu = tuple(sorted(getattr(_TUNING, "kw", {}).items()))
+    key = (P, D, L, n_in, n_out, str(device), int(s.cuda_stream), threading.get_ident(), tu)
     w = _WS_CACHE.get(key)
     if w is None:
         if len(_WS_CACHE) > 16:
