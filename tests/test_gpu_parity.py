@@ -940,7 +940,8 @@ def gpu_paired(dev_trees, obs, n_out, L=None):
 
 
 @pytest.mark.parametrize("P,L,n_in,n_out,B", [(1000, 63, 17, 6, 1), (333, 31, 4, 1, 1), (257, 127, 8, 1, 3),
-                                              (70, 63, 17, 6, 5), (5, 15, 2, 1, 1)])
+                                              (70, 63, 17, 6, 5), (5, 15, 2, 1, 1),
+                                              (300_000, 63, 17, 1, 1)])  # several items per lane (refill)
 def test_paired_ieee_bitexact(P, L, n_in, n_out, B):
     pt, _, _ = make_case(1100 + P, P, L, n_in, 1, "ieee", n_out=n_out, modi=0.1 if n_out > 1 else 0.0)
     obs = synth.dataset_X(1100 + P, 1, P * B, n_in, "normal", -2.0, 2.0).reshape(P, B, n_in)
