@@ -299,6 +299,25 @@ def test_slow_path_extreme_operands_bitexact(n_out, full_set):
         assert ok.all(), (strategy, (~ok).sum())
 
 
+def test_plan_cache_across_shapes_and_tunings():
+    """The C-ABI's per-thread plan cache (last 8 plans keyed by shape, mode,
+    strategy, device and tuning): cycling through more shapes than it holds,
+    interleaved with tuning changes, gives the results of the first calls."""
+    shapes = [(300 + 37 * i, 63, 4, 600 + 128 * i) for i in range(10)]
+    cases = []
+    for i, (P, L, n_in, D) in enumerate(shapes):
+        pt, X, y = make_case(1200 + i, P, L, n_in, D, "paper")
+        dt = to_device(pt, L, n_in)
+        cases.append((dt, X, y, gpu_mse(dt, X, y, "auto"), gpu_eval(dt, X, 1, "auto")))
+    for rep in range(2):
+        for k, (dt, X, y, m0, e0) in enumerate(cases[::-1] if rep else cases):
+            with tuning(unit_chunks=2 if (k + rep) % 2 else 0):
+                m = gpu_mse(dt, X, y, "auto")
+            e = gpu_eval(dt, X, 1, "auto")
+            assert np.array_equal(m.view(np.uint64), m0.view(np.uint64)) or np.allclose(m, m0, rtol=1e-12, equal_nan=True)
+            assert np.array_equal(e.view(np.uint32), e0.view(np.uint32))
+
+
 def test_determinism():
     pt, X, y = make_case(500, 500, 63, 4, 4096, "paper")
     dt = to_device(pt, 63, 4)
