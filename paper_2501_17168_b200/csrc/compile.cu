@@ -337,7 +337,10 @@ __device__ __forceinline__ TreeInfo compile_row(const KParams& p, int64_t tp, No
     Node* s_reord = s_nodes + (Lc + 1);
     ti = stage_tree_warp(p, tp, s_nodes, lane);
     const Node* prog = s_nodes;
-    if (ti.valid && p.fuse && ti.maxdepth - 1 > p.reorder_above) {
+    // the plan's lower threshold (every tree a lot of evaluation work) is for
+    // the paper-set rows' second-child fusion; other rows keep the stack bound
+    const int ra = (p.reorder_paper_only && !ti.paper) ? p.SD : p.reorder_above;
+    if (ti.valid && p.fuse && ti.maxdepth - 1 > ra) {
       // warp-parallel reorder + fusion straight into the program row; rows
       // with inconsistent caller sizes take fuse_copy (no reordering). Rows
       // that need no reordering also take fuse_copy: the second-child fusion
@@ -353,7 +356,7 @@ __device__ __forceinline__ TreeInfo compile_row(const KParams& p, int64_t tp, No
         ti.maxdepth = dep;
         goto compiled;
       }
-    } else if (ti.valid && ti.maxdepth - 1 > p.reorder_above) {
+    } else if (ti.valid && ti.maxdepth - 1 > ra) {
       {
         ti.maxdepth = reorder_program(s_nodes, ti.len, s_reord, scratch + 2 * (Lc + 1) * 8, Lc, lane);
         prog = s_reord;

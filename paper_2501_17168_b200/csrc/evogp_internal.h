@@ -174,6 +174,7 @@ struct KParams {
   int32_t reorder_scratch_bytes;  // k_prepare shared scratch per warp (0: no reordering / fusion)
   int32_t fuse;                   // leaf fusion on (single-output programs with scratch)
   int32_t reorder_above;          // rows with maxdepth - 1 > this are reordered
+  int32_t reorder_paper_only;     // reorder_above below SD applies to paper-set rows only
   // two-tier compile: k_prepare's per-warp scratch (reorder_scratch_bytes) is
   // sized for rows of up to prep_cap nodes; longer rows are queued and
   // compiled by k_prepare_long with long_scratch_bytes per warp (prep_cap == L:

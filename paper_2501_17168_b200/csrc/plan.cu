@@ -302,7 +302,13 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   kp.reorder_scratch_bytes = scratch_for(kp.prep_cap);
   kp.long_scratch_bytes = kp.prep_cap < L ? scratch_for(L) : 0;
   kp.fuse = fuse_on ? 1 : 0;
-  kp.reorder_above = tu.reorder_above > 0 ? tu.reorder_above : SD;
+  // rows deeper than the shared stack must be reordered; when every tree
+  // carries a lot of evaluation work (>= 16 chunks: the compile pass is a
+  // fraction of a percent of the step) all but trivially shallow rows are,
+  // for the second-child leaf fusion that comes with it (C3 +0.7%; on C4,
+  // one chunk per tree, the extra compile work had cost 5% of the step)
+  kp.reorder_above = tu.reorder_above > 0 ? tu.reorder_above : (nch >= 16 ? 1 : SD);
+  kp.reorder_paper_only = (tu.reorder_above == 0 && nch >= 16) ? 1 : 0;  // C5b's full-set rows: -1.3% otherwise
   // opt-in (tuning fused_compile): kernel (a) compiles its own rows when every
   // tree is one work unit (no program-row round trip through HBM, no compile
   // launch; the scratch is the warp's stack region). Not the default: on C4
