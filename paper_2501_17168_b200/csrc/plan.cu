@@ -169,9 +169,14 @@ int plan_problem(Plan& pl, int64_t P, int32_t L, int64_t D, int32_t n_in, int32_
   // resident-warp target: 32 (the K=8 register limit) once the compile pass
   // reorders deep programs; measured in profiles/sweep_kw_r01.txt
   // (K = 16 kernels hold twice the registers: 20 resident warps for (a), 16 for (b))
+  // kernel (a) with every tree one chunk (C4: D = 256): the compile pass is a
+  // third of the step, and 24 warps leave 8 stack slots instead of 5, so far
+  // fewer rows need reordering — the kernel loses 11%, the step gains 3%
+  // (C4 3.94 -> 4.07e12 GPops/s; with 4 chunks per tree, C2, 32 warps stay best)
+  const bool one_chunk = strategy == EVOGP_STRATEGY_INTER && !multi && K == 8 && D <= 32 * K;
   int target_warps = tu.target_warps > 0 ? std::max(4, std::min(64, tu.target_warps))
                                          : (K >= 16 ? (strategy == EVOGP_STRATEGY_INTER ? 20 : 16)
-                                                    : (K == 8 && multi ? 16 : 32));
+                                                    : (K == 8 && multi ? 16 : (one_chunk ? 24 : 32)));
   const int warps = strategy == EVOGP_STRATEGY_INTER ? kInterWarps : kIntraWarps;
   const int64_t chunk = 32 * K;
   const int64_t nch = (D + chunk - 1) / chunk;
